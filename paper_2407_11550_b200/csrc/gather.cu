@@ -1,0 +1,147 @@
+// gather.cu -- K3 copy half: pack kept K/V rows into the flattened varlen cache.
+//
+// Replaces the compaction loop of evict_layer (policies.hpp:273-290: kept outside
+// rows in original order, then the m window rows) and select_and_compact
+// (flat_cache.hpp:92-120: drop evicted rows, preserve order, offsets = prefix sums).
+// Output planes K,V [rows, d]; segment (p, g) starts at seg_start[p*G+g] with
+// capacity budget_g + m + reserve (reserve = decode appends, SPEC.md:454 notes the
+// reference layout has no slack).  Copies are bit-exact, 16-byte vectorised and
+// coalesced (one row = d*esize bytes = 16 x 16 B for bf16 d=128).
+#include "budget_dev.cuh"
+#include "common.cuh"
+
+namespace adakv_b200 {
+
+namespace {
+
+constexpr int kGatherThreads = 256;
+constexpr int kRowsPerBlock = 64;
+
+// seg_start / seqlens for every (p, g).  Problem bases: uniform budgets give a
+// closed form; per-problem budgets (pyramid kinds) need a prefix over problems,
+// done by one block with a sequential carry over 1024-problem tiles.
+__global__ void layout_kernel(const int32_t* __restrict__ budgets, int64_t P, int64_t G, int64_t m,
+                              int64_t reserve, int64_t layer_budget,
+                              const int64_t* __restrict__ layer_budgets, int32_t* __restrict__ seg_start,
+                              int32_t* __restrict__ seqlens) {
+    __shared__ int64_t carry;
+    __shared__ int64_t tile_sum[1024];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t t0 = 0; t0 < P; t0 += blockDim.x) {
+        const int64_t p = t0 + threadIdx.x;
+        int64_t rows = 0;
+        if (p < P) rows = (layer_budgets ? layer_budgets[p] : layer_budget) + G * reserve;
+        tile_sum[threadIdx.x] = rows;
+        __syncthreads();
+        // inclusive Hillis-Steele scan over the tile
+        for (int o = 1; o < int(blockDim.x); o <<= 1) {
+            const int64_t v = threadIdx.x >= unsigned(o) ? tile_sum[threadIdx.x - o] : 0;
+            __syncthreads();
+            tile_sum[threadIdx.x] += v;
+            __syncthreads();
+        }
+        if (p < P) {
+            int64_t base = carry + tile_sum[threadIdx.x] - rows;
+            for (int64_t g = 0; g < G; ++g) {
+                const int64_t len = budgets[p * G + g] + m;
+                seg_start[p * G + g] = int32_t(base);
+                seqlens[p * G + g] = int32_t(len);
+                base += len + reserve;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += tile_sum[threadIdx.x];
+        __syncthreads();
+    }
+}
+
+template <class V>
+__global__ void __launch_bounds__(kGatherThreads)
+gather_kernel(const V* __restrict__ k, const V* __restrict__ v, int64_t G, int64_t n_rows,
+              int64_t n_o, int64_t m, int64_t vec_per_row, const int32_t* __restrict__ budgets,
+              const int32_t* __restrict__ kept_pos, int64_t kept_stride,
+              const int32_t* __restrict__ seg_start, V* __restrict__ k_cache,
+              V* __restrict__ v_cache) {
+    __shared__ int64_t cum[kMaxSeg + 1];   // cumulative (budget + m) per group
+    __shared__ int64_t bcum[kMaxSeg + 1];  // cumulative budget per group (kept_pos offset)
+    const int64_t p = blockIdx.y;
+    if (threadIdx.x == 0) {
+        cum[0] = 0;
+        bcum[0] = 0;
+        for (int64_t g = 0; g < G; ++g) {
+            const int64_t b = budgets[p * G + g];
+            cum[g + 1] = cum[g] + b + m;
+            bcum[g + 1] = bcum[g] + b;
+        }
+    }
+    __syncthreads();
+    const int64_t total = cum[G];
+    const int64_t r0 = int64_t(blockIdx.x) * kRowsPerBlock;
+    const int64_t r1 = min(r0 + int64_t(kRowsPerBlock), total);
+    const int64_t items = (r1 - r0) * vec_per_row;
+    for (int64_t it = threadIdx.x; it < items; it += kGatherThreads) {
+        const int64_t r = r0 + it / vec_per_row, c = it % vec_per_row;
+        int64_t g = 0;
+        while (cum[g + 1] <= r) ++g;
+        const int64_t rin = r - cum[g];
+        const int64_t b = bcum[g + 1] - bcum[g];
+        const int64_t src_row = rin < b ? int64_t(kept_pos[p * kept_stride + bcum[g] + rin]) : n_o + (rin - b);
+        const int64_t src = ((p * G + g) * n_rows + src_row) * vec_per_row + c;
+        const int64_t dst = (int64_t(seg_start[p * G + g]) + rin) * vec_per_row + c;
+        k_cache[dst] = k[src];
+        v_cache[dst] = v[src];
+    }
+}
+
+}  // namespace
+
+adakv_status launch_layout(const int32_t* budgets, int64_t P, int64_t G, int64_t m, int64_t reserve,
+                           int64_t layer_budget, const int64_t* layer_budgets, int32_t* seg_start,
+                           int32_t* seqlens, cudaStream_t stream) {
+    if (G > kMaxSeg) return fail(ADAKV_UNSUPPORTED, "gather: more than 64 KV groups");
+    layout_kernel<<<1, 1024, 0, stream>>>(budgets, P, G, m, reserve, layer_budget, layer_budgets,
+                                          seg_start, seqlens);
+    ADAKV_CUDA_TRY(cudaGetLastError());
+    return ADAKV_OK;
+}
+
+adakv_status launch_gather(adakv_dtype dt, const adakv_layer_shape& s, int64_t max_rows,
+                           const void* k, const void* v, const int32_t* budgets,
+                           const int32_t* kept_pos, int64_t kept_stride, const int32_t* seg_start,
+                           void* k_cache, void* v_cache, cudaStream_t stream) {
+    const int64_t P = s.problems, G = s.kv_groups, d = s.head_dim;
+    const int64_t row_bytes = d * int64_t(dtype_size(dt));
+    const dim3 grid(unsigned(ceil_div(max_rows, kRowsPerBlock)), unsigned(P));
+    if (grid.x == 0 || P == 0) return ADAKV_OK;
+    const bool aligned16 = row_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(k) % 16 == 0) &&
+                           (reinterpret_cast<uintptr_t>(v) % 16 == 0) &&
+                           (reinterpret_cast<uintptr_t>(k_cache) % 16 == 0) &&
+                           (reinterpret_cast<uintptr_t>(v_cache) % 16 == 0);
+    const int64_t n_rows = s.outside + s.window;
+    if (aligned16) {
+        gather_kernel<int4><<<grid, kGatherThreads, 0, stream>>>(
+            static_cast<const int4*>(k), static_cast<const int4*>(v), G, n_rows, s.outside, s.window,
+            row_bytes / 16, budgets, kept_pos, kept_stride, seg_start, static_cast<int4*>(k_cache),
+            static_cast<int4*>(v_cache));
+    } else if (row_bytes % 8 == 0) {
+        gather_kernel<int2><<<grid, kGatherThreads, 0, stream>>>(
+            static_cast<const int2*>(k), static_cast<const int2*>(v), G, n_rows, s.outside, s.window,
+            row_bytes / 8, budgets, kept_pos, kept_stride, seg_start, static_cast<int2*>(k_cache),
+            static_cast<int2*>(v_cache));
+    } else if (row_bytes % 4 == 0) {
+        gather_kernel<int><<<grid, kGatherThreads, 0, stream>>>(
+            static_cast<const int*>(k), static_cast<const int*>(v), G, n_rows, s.outside, s.window,
+            row_bytes / 4, budgets, kept_pos, kept_stride, seg_start, static_cast<int*>(k_cache),
+            static_cast<int*>(v_cache));
+    } else {
+        gather_kernel<uint16_t><<<grid, kGatherThreads, 0, stream>>>(
+            static_cast<const uint16_t*>(k), static_cast<const uint16_t*>(v), G, n_rows, s.outside,
+            s.window, row_bytes / 2, budgets, kept_pos, kept_stride, seg_start,
+            static_cast<uint16_t*>(k_cache), static_cast<uint16_t*>(v_cache));
+    }
+    ADAKV_CUDA_TRY(cudaGetLastError());
+    return ADAKV_OK;
+}
+
+}  // namespace adakv_b200

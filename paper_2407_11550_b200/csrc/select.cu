@@ -1,0 +1,518 @@
+// select.cu -- K2/K3 selection: layer-wide radix select -> adaptive budgets ->
+// safeguard/repair -> per-segment radix select -> keep mask + kept positions.
+//
+// Replaces adaptive_allocation (budget.hpp:118-140: layer-wide top-`total` over the
+// concatenated segments, ordered (score desc, head asc, pos asc) = flat order),
+// safeguard_blend + apportion (145-158, 45-93), uniform_allocation (103-113),
+// repair_zero_budgets (policies.hpp:178-196), topk_decision (80-93: ties to the
+// lowest position) and streaming_llm_decision (159-165).
+//
+// Design (B200): one thread-block cluster of CS <= 8 CTAs per problem, 1024
+// threads each; CTA r owns a contiguous slice of the problem's flattened scores.
+// Keys are the scores' bit patterns mapped to an order-preserving unsigned integer
+// (-0 canonicalised to +0), selected MSB-first with 8-bit digits: per-CTA
+// per-segment shared-memory histograms (warp-aggregated with match.any), summed
+// across the cluster through distributed shared memory, one cluster barrier per
+// digit (double-buffered histograms).  Exactness: the threshold key T and the
+// number of T-equal elements to take are integers, and "lowest flat index wins a
+// tie" is realised by ballot-ranked prefix counts in flat order, so budgets, keep
+// masks and kept positions are bit-identical to the reference on identical scores.
+#include <cooperative_groups.h>
+
+#include "select.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace adakv_b200 {
+
+
+
+namespace {
+
+constexpr int kSelThreads = 1024;
+constexpr int kWarps = kSelThreads / 32;
+
+enum SegMode : int { MODE_NONE = 0, MODE_ALL = 1, MODE_THRESH = 2, MODE_STREAM = 3 };
+
+template <class F> struct KeyOf;
+template <> struct KeyOf<float> {
+    using type = uint32_t;
+    static constexpr int kBits = 32;
+    __device__ static uint32_t get(float x) {
+        uint32_t b = __float_as_uint(x);
+        if (b == 0x80000000u) b = 0u;  // -0 == +0 (the reference compares with !=, >)
+        return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    }
+};
+template <> struct KeyOf<double> {
+    using type = unsigned long long;
+    static constexpr int kBits = 64;
+    __device__ static unsigned long long get(double x) {
+        unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+        if (b == 0x8000000000000000ull) b = 0ull;
+        return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+    }
+};
+
+struct BinPick {
+    int bin;
+    int64_t cum_above;
+};
+
+// Warp-cooperative: in a 256-bin histogram find the bin holding the krem-th
+// largest element (krem >= 1), scanning bins from high to low.
+__device__ __forceinline__ BinPick find_bin(const uint32_t* h, int64_t krem, int lane) {
+    int64_t s8 = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s8 += h[lane * 8 + i];
+    int64_t suf = s8;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_down_sync(0xffffffffu, suf, o);
+        if (lane + o < 32) suf += t;
+    }
+    int64_t next = __shfl_down_sync(0xffffffffu, suf, 1);
+    if (lane == 31) next = 0;
+    const unsigned hit = __ballot_sync(0xffffffffu, suf >= krem && next < krem);
+    const int L = hit ? __ffs(hit) - 1 : 0;
+    int bin = 0;
+    int64_t cum = 0;
+    if (lane == L) {
+        cum = next;
+        bin = L * 8;
+        for (int i = 7; i >= 0; --i) {
+            const int64_t c = h[L * 8 + i];
+            if (cum + c >= krem) {
+                bin = L * 8 + i;
+                break;
+            }
+            cum += c;
+        }
+    }
+    bin = __shfl_sync(0xffffffffu, bin, L);
+    cum = __shfl_sync(0xffffffffu, cum, L);
+    return {bin, cum};
+}
+
+template <class F>
+__global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams prm) {
+    using KT = typename KeyOf<F>::type;
+    constexpr int kBits = KeyOf<F>::kBits;
+    constexpr int kPasses = kBits / 8;
+    cg::cluster_group cluster = cg::this_cluster();
+    const unsigned CS = cluster.num_blocks();
+    const unsigned rank = cluster.block_rank();
+    const int64_t p = blockIdx.x / CS;
+    const int S = prm.S;
+    const int64_t N = prm.N;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const F* sc = static_cast<const F*>(prm.scores) + p * N;
+    const int64_t lo = N * rank / CS, hi = N * (rank + 1) / CS;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);     // [2][S][256]
+    uint32_t* agg = hist + 2 * S * 256;                          // [S][256]
+    uint32_t* hist0 = agg + S * 256;                             // [S][256]
+    uint32_t* wcnt = hist0 + S * 256;                            // [kWarps][S][2]
+    int64_t* wkept = reinterpret_cast<int64_t*>(wcnt + kWarps * S * 2);  // [kWarps][S]
+    int64_t* weqb = wkept + kWarps * S;                                  // [kWarps][S]
+
+    __shared__ uint32_t ccnt[kMaxSeg][2];  // this CTA's (gt, eq) per segment
+    __shared__ KT seg_prefix[kMaxSeg];
+    __shared__ int64_t seg_krem[kMaxSeg], seg_gt[kMaxSeg], seg_need[kMaxSeg];
+    __shared__ KT seg_T[kMaxSeg];
+    __shared__ int seg_mode[kMaxSeg], seg_active[kMaxSeg];
+    __shared__ int64_t seg_sink[kMaxSeg], seg_recent[kMaxSeg], seg_eqb[kMaxSeg];
+    __shared__ uint64_t b_raw[kMaxSeg], b_fin[kMaxSeg], b_caps[kMaxSeg];
+    __shared__ double quotas[kMaxSeg];
+    __shared__ int64_t wkept_before[kWarps];
+    __shared__ KT g_T;
+    __shared__ int64_t g_take, g_k;
+    __shared__ int any_active, have_hist0;
+    __shared__ uint32_t s_err;
+
+    if (tid == 0) {
+        s_err = 0;
+        have_hist0 = 0;
+        g_k = prm.totals ? prm.totals[p] : prm.total;
+    }
+    for (int s = tid; s < S; s += kSelThreads) {
+        seg_gt[s] = 0;
+        b_caps[s] = uint64_t(prm.off[s + 1] - prm.off[s]);
+    }
+    __syncthreads();
+
+    // One radix digit over all segments with seg_active[s] set: per-segment
+    // histograms of elements matching that segment's prefix, cluster-summed into agg.
+    int buf = 0;  // histogram double buffer; toggled only by a pass that used it
+    auto radix_pass = [&](int pass) {
+        const int shift = kBits - 8 * (pass + 1);
+        const KT mask = pass == 0 ? KT(0) : (~KT(0)) << (kBits - 8 * pass);
+        uint32_t* hb = hist + buf * S * 256;
+        for (int i = tid; i < S * 256; i += kSelThreads) hb[i] = 0;
+        __syncthreads();
+        for (int s = 0; s < S; ++s) {
+            if (!seg_active[s]) continue;
+            const int64_t a = max(lo, prm.off[s]), b = min(hi, prm.off[s + 1]);
+            const KT pre = seg_prefix[s];
+            for (int64_t base = a; base < b; base += kSelThreads) {
+                const int64_t e = base + tid;
+                int key = -1;
+                if (e < b) {
+                    const KT u = KeyOf<F>::get(sc[e]);
+                    if ((u & mask) == pre) key = int((u >> shift) & 0xFF);
+                }
+                const unsigned peers = __match_any_sync(0xffffffffu, key);
+                if (key >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hb[s * 256 + key], __popc(peers));
+            }
+        }
+        cluster.sync();
+        for (int i = tid; i < S * 256; i += kSelThreads) {
+            uint32_t t = 0;
+            for (unsigned r = 0; r < CS; ++r) t += cluster.map_shared_rank(hb, r)[i];
+            agg[i] = t;
+        }
+        __syncthreads();
+        buf ^= 1;
+    };
+
+    // ---------------- Phase A: layer-wide top-k (Algorithm 1, budget.hpp:118-140)
+    const bool adaptive = prm.alloc_mode == ADAKV_ALLOC_ADAPTIVE;
+    if (adaptive && g_k > 0) {
+        __shared__ int64_t g_krem;
+        __shared__ KT g_prefix;
+        if (tid == 0) {
+            g_krem = g_k;
+            g_prefix = 0;
+        }
+        for (int s = tid; s < S; s += kSelThreads) seg_active[s] = 1;
+        __syncthreads();
+        for (int pass = 0; pass < kPasses; ++pass) {
+            for (int s = tid; s < S; s += kSelThreads) seg_prefix[s] = g_prefix;
+            __syncthreads();
+            radix_pass(pass);
+            if (pass == 0) {
+                for (int i = tid; i < S * 256; i += kSelThreads) hist0[i] = agg[i];
+                if (tid == 0) have_hist0 = 1;
+            }
+            __shared__ int g_bin;
+            __shared__ uint32_t gsum[256];
+            for (int b = tid; b < 256; b += kSelThreads) {
+                uint32_t t = 0;
+                for (int s = 0; s < S; ++s) t += agg[s * 256 + b];
+                gsum[b] = t;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                const BinPick bp = find_bin(gsum, g_krem, lane);
+                if (lane == 0) {
+                    g_bin = bp.bin;
+                    g_krem -= bp.cum_above;
+                    g_prefix |= KT(bp.bin) << (kBits - 8 * (pass + 1));
+                }
+            }
+            __syncthreads();
+            // elements above the chosen bin are definitely selected
+            for (int s = warp; s < S; s += kWarps) {
+                int64_t t = 0;
+                for (int b = g_bin + 1 + lane; b < 256; b += 32) t += agg[s * 256 + b];
+                for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                if (lane == 0) {
+                    seg_gt[s] += t;
+                    if (pass == kPasses - 1) seg_need[s] = agg[s * 256 + g_bin];  // eq_s
+                }
+            }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            g_T = g_prefix;
+            g_take = g_krem;
+            int64_t rem = g_krem;
+            for (int s = 0; s < S; ++s) {
+                const int64_t take = seg_need[s] < rem ? seg_need[s] : rem;
+                rem -= take;
+                seg_need[s] = take;  // T-equal elements of segment s inside the layer-wide top-k
+                b_raw[s] = uint64_t(seg_gt[s] + take);
+            }
+        }
+    } else if (adaptive && tid == 0) {
+        for (int s = 0; s < S; ++s) b_raw[s] = 0;
+    }
+    __syncthreads();
+
+    // ---------------- Phase C: allocation (one thread, redundantly per CTA, bit-exact fp64)
+    if (tid == 0) {
+        uint32_t e = 0;
+        const uint64_t k = uint64_t(g_k);
+        if (adaptive) {
+            if (prm.blend) e |= safeguard_dev(b_raw, k, S, prm.alpha, b_caps, quotas, b_fin);
+            else
+                for (int s = 0; s < S; ++s) b_fin[s] = b_raw[s];
+        } else if (prm.alloc_mode == ADAKV_ALLOC_UNIFORM) {
+            e |= uniform_dev(k, S, b_caps, quotas, b_fin);
+        } else {
+            for (int s = 0; s < S; ++s) {
+                const int64_t b = prm.budgets[p * S + s];
+                if (b < 0 || uint64_t(b) > b_caps[s]) e |= ERR_BUDGET;
+                b_fin[s] = b < 0 ? 0 : (uint64_t(b) > b_caps[s] ? b_caps[s] : uint64_t(b));
+            }
+        }
+        if (!e && prm.repair) e |= repair_dev(b_fin, b_caps, S);
+        any_active = 0;
+        for (int s = 0; s < S; ++s) {
+            const int64_t b = int64_t(b_fin[s]), n = int64_t(b_caps[s]);
+            seg_active[s] = 0;
+            if (e) {
+                seg_mode[s] = MODE_NONE;
+            } else if (prm.streaming) {
+                seg_mode[s] = MODE_STREAM;
+                seg_sink[s] = prm.sink < b ? prm.sink : b;
+                seg_recent[s] = b - seg_sink[s];
+            } else if (b == 0) {
+                seg_mode[s] = MODE_NONE;
+            } else if (b == n) {
+                seg_mode[s] = MODE_ALL;
+            } else if (adaptive && g_k > 0 && b_fin[s] == b_raw[s]) {
+                // per-segment top-b == the layer-wide selection restricted to s
+                seg_mode[s] = MODE_THRESH;
+                seg_T[s] = g_T;
+            } else {
+                seg_mode[s] = MODE_THRESH;
+                seg_active[s] = 1;
+                seg_prefix[s] = 0;
+                seg_krem[s] = b;
+                any_active = 1;
+            }
+        }
+        s_err = e;
+        if (e && rank == 0) atomicOr(prm.err, e);
+    }
+    __syncthreads();
+    if (rank == 0) {
+        for (int s = tid; s < S; s += kSelThreads) {
+            prm.budgets[p * S + s] = int32_t(b_fin[s]);
+            if (adaptive && prm.raw_counts) prm.raw_counts[p * S + s] = int32_t(b_raw[s]);
+        }
+    }
+
+    // ---------------- Phase D: per-segment top-b (topk_decision, policies.hpp:80-93)
+    if (any_active) {
+        for (int pass = 0; pass < kPasses; ++pass) {
+            if (pass == 0 && have_hist0) {
+                for (int i = tid; i < S * 256; i += kSelThreads) agg[i] = hist0[i];
+                __syncthreads();
+            } else {
+                radix_pass(pass);
+            }
+            for (int s = warp; s < S; s += kWarps) {
+                if (!seg_active[s]) continue;
+                const BinPick bp = find_bin(agg + s * 256, seg_krem[s], lane);
+                if (lane == 0) {
+                    seg_krem[s] -= bp.cum_above;
+                    seg_prefix[s] |= KT(bp.bin) << (kBits - 8 * (pass + 1));
+                }
+            }
+            __syncthreads();
+        }
+        for (int s = tid; s < S; s += kSelThreads)
+            if (seg_active[s]) {
+                seg_T[s] = seg_prefix[s];
+                seg_need[s] = seg_krem[s];
+            }
+    }
+    __syncthreads();
+
+    // ---------------- Phase E: keep mask and kept positions in flat order
+    const int64_t wlo = lo + (hi - lo) * warp / kWarps, whi = lo + (hi - lo) * (warp + 1) / kWarps;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int i = tid; i < kWarps * S * 2; i += kSelThreads) wcnt[i] = 0;
+    __syncthreads();
+    for (int s = 0; s < S; ++s) {
+        const int64_t a = max(wlo, prm.off[s]), b = min(whi, prm.off[s + 1]);
+        if (a >= b) continue;
+        const int mode = seg_mode[s];
+        uint32_t gt = 0, eq = 0;
+        if (mode == MODE_THRESH) {
+            const KT T = seg_T[s];
+            for (int64_t base = a; base < b; base += 32) {
+                const int64_t e = base + lane;
+                KT u = 0;
+                if (e < b) u = KeyOf<F>::get(sc[e]);
+                gt += __popc(__ballot_sync(0xffffffffu, e < b && u > T));
+                eq += __popc(__ballot_sync(0xffffffffu, e < b && u == T));
+            }
+        } else if (mode == MODE_ALL) {
+            gt = uint32_t(b - a);
+        } else if (mode == MODE_STREAM) {
+            const int64_t n = prm.off[s + 1] - prm.off[s];
+            const int64_t pa = a - prm.off[s], pb = b - prm.off[s];
+            const int64_t s_hi = seg_sink[s], r_lo = n - seg_recent[s];
+            const int64_t c1 = max(int64_t(0), min(pb, s_hi) - pa);
+            const int64_t c2 = max(int64_t(0), pb - max(pa, r_lo));
+            gt = uint32_t(c1 + c2);
+        }
+        if (lane == 0) {
+            wcnt[(warp * S + s) * 2 + 0] = gt;
+            wcnt[(warp * S + s) * 2 + 1] = eq;
+        }
+    }
+    __syncthreads();
+    for (int s = tid; s < S; s += kSelThreads) {
+        uint32_t gt = 0, eq = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            gt += wcnt[(w * S + s) * 2 + 0];
+            eq += wcnt[(w * S + s) * 2 + 1];
+        }
+        ccnt[s][0] = gt;
+        ccnt[s][1] = eq;
+    }
+    cluster.sync();
+    // cross-CTA prefix: T-equal elements and kept elements before this CTA
+    __shared__ int64_t cta_kept_before;
+    __shared__ int64_t seg_kept_before[kMaxSeg];
+    for (int s = tid; s < S; s += kSelThreads) {
+        int64_t eqb = 0, kept = 0;
+        const int64_t need = seg_mode[s] == MODE_THRESH ? seg_need[s] : 0;
+        for (unsigned r = 0; r < rank; ++r) {
+            const uint32_t* rc = cluster.map_shared_rank(&ccnt[0][0], r);
+            const int64_t g = rc[s * 2 + 0], q = rc[s * 2 + 1];
+            const int64_t t = need - eqb;
+            kept += g + (t <= 0 ? 0 : (t < q ? t : q));
+            eqb += q;
+        }
+        seg_eqb[s] = eqb;
+        seg_kept_before[s] = kept;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int64_t t = 0;
+        for (int s = 0; s < S; ++s) t += seg_kept_before[s];
+        cta_kept_before = t;
+    }
+    for (int s = tid; s < S; s += kSelThreads) {
+        int64_t eqb = seg_eqb[s];
+        const int64_t need = seg_mode[s] == MODE_THRESH ? seg_need[s] : 0;
+        for (int w = 0; w < kWarps; ++w) {
+            const int64_t g = wcnt[(w * S + s) * 2 + 0], q = wcnt[(w * S + s) * 2 + 1];
+            const int64_t t = need - eqb;
+            wkept[w * S + s] = g + (t <= 0 ? 0 : (t < q ? t : q));
+            weqb[w * S + s] = eqb;
+            eqb += q;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int64_t run = cta_kept_before;
+        for (int w = 0; w < kWarps; ++w) {
+            wkept_before[w] = run;
+            for (int s = 0; s < S; ++s) run += wkept[w * S + s];
+        }
+    }
+    __syncthreads();
+    {
+        int64_t run_kept = wkept_before[warp];
+        uint8_t* keep_out = prm.keep ? prm.keep + p * N : nullptr;
+        int32_t* kp = prm.kept_pos ? prm.kept_pos + p * prm.kept_stride : nullptr;
+        for (int s = 0; s < S; ++s) {
+            const int64_t a = max(wlo, prm.off[s]), b = min(whi, prm.off[s + 1]);
+            if (a >= b) continue;
+            const int mode = seg_mode[s];
+            const KT T = seg_T[s];
+            const int64_t need = seg_need[s];
+            const int64_t n = prm.off[s + 1] - prm.off[s];
+            int64_t run_eq = weqb[warp * S + s];
+            for (int64_t base = a; base < b; base += 32) {
+                const int64_t e = base + lane;
+                const bool valid = e < b;
+                const int64_t pos = e - prm.off[s];
+                bool keep = false;
+                if (mode == MODE_THRESH) {
+                    KT u = 0;
+                    if (valid) u = KeyOf<F>::get(sc[e]);
+                    const bool is_eq = valid && u == T;
+                    const unsigned beq = __ballot_sync(0xffffffffu, is_eq);
+                    const int64_t eqr = run_eq + __popc(beq & lt);
+                    keep = valid && (u > T || (is_eq && eqr < need));
+                    run_eq += __popc(beq);
+                } else if (mode == MODE_ALL) {
+                    keep = valid;
+                } else if (mode == MODE_STREAM) {
+                    keep = valid && (pos < seg_sink[s] || pos >= n - seg_recent[s]);
+                }
+                const unsigned bk = __ballot_sync(0xffffffffu, keep);
+                if (keep && kp) kp[run_kept + __popc(bk & lt)] = int32_t(pos);
+                if (valid && keep_out) keep_out[e] = keep ? 1 : 0;
+                run_kept += __popc(bk);
+            }
+        }
+    }
+    cluster.sync();  // keep peer shared memory alive until every CTA is done reading it
+}
+
+}  // namespace
+
+size_t select_smem_bytes(int S) {
+    return size_t(4) * (2 * S * 256 + S * 256 + S * 256 + kWarps * S * 2) + size_t(8) * 2 * kWarps * S;
+}
+
+adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStream_t stream) {
+    if (P == 0) return ADAKV_OK;
+    const int64_t per_cta = 16384;
+    int CS = int(ceil_div(prm.N, per_cta));
+    CS = CS < 1 ? 1 : (CS > 8 ? 8 : CS);
+    const size_t smem = select_smem_bytes(prm.S);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(P * CS));
+    cfg.blockDim = dim3(kSelThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(CS);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (key64) {
+        ADAKV_CUDA_TRY(cudaFuncSetAttribute(select_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel<double>, prm));
+    } else {
+        ADAKV_CUDA_TRY(cudaFuncSetAttribute(select_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel<float>, prm));
+    }
+    return ADAKV_OK;
+}
+
+// ---------------------------------------------------------------- standalone budget kernels
+__global__ void budget_kernel(int op, const double* quotas_in, const int64_t* a_in, int64_t h,
+                              int64_t total, double alpha, double bmax, double bmin,
+                              const int64_t* caps_in, int64_t* out, double* quotas,
+                              uint64_t* caps, uint64_t* tmp_a, uint64_t* tmp_o, uint32_t* err) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int64_t i = 0; i < h; ++i) caps[i] = caps_in ? uint64_t(caps_in[i]) : kAmpleCap;
+    uint32_t e = 0;
+    switch (op) {
+        case 0:  // apportion
+            for (int64_t i = 0; i < h; ++i) quotas[i] = quotas_in[i];
+            e = apportion_dev(quotas, int(h), uint64_t(total), caps, tmp_o);
+            break;
+        case 1:  // uniform
+            e = uniform_dev(uint64_t(total), int(h), caps, quotas, tmp_o);
+            break;
+        case 2:  // safeguard
+            for (int64_t i = 0; i < h; ++i) tmp_a[i] = uint64_t(a_in[i]);
+            e = safeguard_dev(tmp_a, uint64_t(total), int(h), alpha, caps, quotas, tmp_o);
+            break;
+        case 3:  // repair (in place)
+            for (int64_t i = 0; i < h; ++i) tmp_o[i] = uint64_t(a_in[i]);
+            e = repair_dev(tmp_o, caps, int(h));
+            break;
+        case 4:  // pyramid
+            e = pyramid_dev(uint64_t(total), int(h), bmax, bmin, quotas, caps, tmp_o);
+            break;
+    }
+    *err = e;
+    for (int64_t i = 0; i < h; ++i) out[i] = int64_t(tmp_o[i]);
+}
+
+}  // namespace adakv_b200

@@ -1,0 +1,28 @@
+// select.cuh -- parameters of the cluster selection kernel (select.cu).
+#pragma once
+
+#include "budget_dev.cuh"
+
+namespace adakv_b200 {
+
+struct SelParams {
+    int64_t off[kMaxSeg + 1];  // segment offsets within a problem (S + 1 entries)
+    int S;
+    int64_t N;                 // elements per problem (off[S])
+    int alloc_mode, blend, repair, streaming;
+    double alpha;
+    int64_t sink;
+    int64_t total;             // outside budget (uniform over problems) ...
+    const int64_t* totals;     // ... or per problem (device), overrides total
+    const void* scores;
+    int32_t* raw_counts;
+    int32_t* budgets;
+    uint8_t* keep;
+    int32_t* kept_pos;
+    int64_t kept_stride;
+    uint32_t* err;
+};
+
+adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStream_t stream);
+
+}  // namespace adakv_b200

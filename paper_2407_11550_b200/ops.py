@@ -1,0 +1,300 @@
+"""torch-tensor front end over the C ABI (include/adakv_b200.h).
+
+Every function launches on torch's current CUDA stream and calls straight into
+lib/libadakv_b200.so; nothing here computes on the CPU.  Names follow the
+reference (adakv::evict_layer, window_scores, adaptive_allocation, ...), see
+the C header for the file:line each entry point replaces.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+_DT = {torch.bfloat16: L.BF16, torch.float32: L.F32, torch.float64: L.F64}
+
+
+def _dt(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise L.InvalidArgument(1, f"unsupported dtype {t.dtype}") from None
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise L.InvalidArgument(1, "tensors must live on a CUDA device (no CPU path)")
+        if t is not None and not t.is_contiguous():
+            raise L.InvalidArgument(1, "tensors must be contiguous")
+
+
+_ws_cache: dict = {}
+
+
+def workspace(nbytes: int, device, key="default") -> torch.Tensor:
+    """Cached uint8 workspace (zero-initialised on first allocation)."""
+    k = (str(device), key)
+    t = _ws_cache.get(k)
+    if t is None or t.numel() < nbytes:
+        t = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _ws_cache[k] = t
+    return t
+
+
+def policy_config(kind="ada_snapkv", pool_kernel=7, alpha=0.2, sink_tokens=4, gqa_group_size=1,
+                  scale=True, window_size=32) -> L.PolicyConfig:
+    return L.PolicyConfig(L.KINDS[kind] if isinstance(kind, str) else int(kind), int(bool(scale)),
+                          int(window_size), int(pool_kernel), float(alpha), int(sink_tokens),
+                          int(gqa_group_size))
+
+
+def layer_shape(P, H, G, m, n_o, d) -> L.LayerShape:
+    return L.LayerShape(int(P), int(H), int(G), int(m), int(n_o), int(d))
+
+
+@dataclass
+class CompressedCache:
+    """The flattened variable-length cache (flat_cache.hpp:24-36) on the device.
+
+    Segment (p, g) holds rows [seg_start, seg_start + seqlens) of k/v: kept outside
+    rows in original order, then the m window rows (policies.hpp:273-290);
+    capacity per segment = budgets + m + reserve.
+    """
+    k: torch.Tensor
+    v: torch.Tensor
+    seg_start: torch.Tensor  # int32 [P*G]
+    seqlens: torch.Tensor    # int32 [P*G]
+    budgets: torch.Tensor    # int32 [P*G] outside budget per group (BudgetAllocation)
+    P: int
+    H: int
+    G: int
+    m: int
+    d: int
+    reserve: int
+    layer_budget: int
+    scores: torch.Tensor | None = None  # [P, G, n_o] pooled group scores
+    keep: torch.Tensor | None = None    # uint8 [P, G, n_o] decision
+
+    @property
+    def max_rows(self) -> int:
+        return self.layer_budget + self.reserve  # any segment fits in budget_total + reserve
+
+    def segment(self, p: int, g: int):
+        s = int(self.seg_start[p * self.G + g])
+        n = int(self.seqlens[p * self.G + g])
+        return self.k[s:s + n], self.v[s:s + n]
+
+
+def compress(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layer_budget: int, kind="ada_snapkv",
+             pool_kernel=7, alpha=0.2, sink_tokens=4, scale=True, reserve=0, layer_budgets=None,
+             return_scores=False, return_keep=False, out: CompressedCache | None = None,
+             ws: torch.Tensor | None = None) -> CompressedCache:
+    """evict_layer (policies.hpp:204-293) for P problems at once.
+
+    q [P, H, m, d]; k, v [P, G, n, d] with the observation window in the last m rows.
+    layer_budget counts unique KV entries per problem, window included.
+    layer_budgets: optional int64 CUDA tensor [P] (per-problem budgets, pyramid kinds).
+    """
+    _need_cuda(q, k, v)
+    P, H, m, d = q.shape
+    P2, G, n, d2 = k.shape
+    if P2 != P or d2 != d or v.shape != k.shape or k.dtype != q.dtype or v.dtype != q.dtype:
+        raise L.InvalidArgument(1, "compress: q/k/v shape or dtype mismatch")
+    n_o = n - m
+    dt = _dt(q)
+    shape = layer_shape(P, H, G, m, n_o, d)
+    cfg = policy_config(kind, pool_kernel, alpha, sink_tokens, H // G if G else 1, scale, m)
+    lib = L.lib()
+    if layer_budgets is not None:
+        lb_host = layer_budgets.detach().cpu().numpy().astype(np.int64)
+        rows = int(lb_host.sum()) + P * G * reserve
+        lbmax = int(lb_host.max()) if lb_host.size else 0
+    else:
+        rows = P * (layer_budget + G * reserve)
+        lbmax = layer_budget
+    dev = q.device
+    acc_dtype = torch.float64 if q.dtype == torch.float64 else torch.float32
+    if out is None:
+        out = CompressedCache(
+            k=torch.empty((max(rows, 1), d), dtype=q.dtype, device=dev),
+            v=torch.empty((max(rows, 1), d), dtype=q.dtype, device=dev),
+            seg_start=torch.empty(P * G, dtype=torch.int32, device=dev),
+            seqlens=torch.empty(P * G, dtype=torch.int32, device=dev),
+            budgets=torch.empty(P * G, dtype=torch.int32, device=dev),
+            P=P, H=H, G=G, m=m, d=d, reserve=reserve, layer_budget=lbmax,
+            scores=torch.empty((P, G, n_o), dtype=acc_dtype, device=dev) if return_scores else None,
+            keep=torch.empty((P, G, n_o), dtype=torch.uint8, device=dev) if return_keep else None)
+    nbytes = C.c_size_t()
+    L.check(lib.adakv_compress_workspace(dt, C.byref(shape), C.byref(cfg), C.byref(nbytes)))
+    if ws is None:
+        ws = workspace(nbytes.value, dev, "compress")
+    L.check(lib.adakv_compress(dt, C.byref(shape), C.byref(cfg), int(layer_budget), _p(layer_budgets), _p(q),
+                               _p(k), _p(v), int(reserve), _p(out.k), _p(out.v), _p(out.seg_start),
+                               _p(out.seqlens), _p(out.budgets), _p(out.scores), _p(out.keep), _p(ws),
+                               ws.numel(), _stream()))
+    return out
+
+
+def window_scores(q: torch.Tensor, k: torch.Tensor, pool_kernel=7, scale=True, head_scores=False,
+                  ws: torch.Tensor | None = None):
+    """window_scores (policies.hpp:119-132) for every head + group_mean_scores (136-156).
+
+    q [P, H, m, d]; k [P, G, n, d] (outside keys are rows [0, n - m)).
+    Returns group scores [P, G, n_o] (and per-head scores [P, H, n_o] if asked).
+    """
+    _need_cuda(q, k)
+    P, H, m, d = q.shape
+    _, G, n, _ = k.shape
+    n_o = n - m
+    dt = _dt(q)
+    shape = layer_shape(P, H, G, m, n_o, d)
+    acc = torch.float64 if q.dtype == torch.float64 else torch.float32
+    gs = torch.empty((P, G, n_o), dtype=acc, device=q.device)
+    hs = torch.empty((P, H, n_o), dtype=acc, device=q.device) if head_scores else None
+    lib = L.lib()
+    nbytes = C.c_size_t()
+    L.check(lib.adakv_window_scores_workspace(dt, C.byref(shape), C.byref(nbytes)))
+    if ws is None:
+        ws = workspace(nbytes.value * 2, q.device, "scores")
+    L.check(lib.adakv_window_scores(dt, C.byref(shape), int(pool_kernel), int(bool(scale)), _p(q), _p(k), _p(hs),
+                                    _p(gs), _p(ws), ws.numel(), _stream()))
+    return (gs, hs) if head_scores else gs
+
+
+def segmented_select(scores: torch.Tensor, seg_off, total=0, mode="adaptive", blend=False, alpha=1.0,
+                     repair=False, streaming=False, sink_tokens=4, budgets: torch.Tensor | None = None,
+                     totals: torch.Tensor | None = None, want_keep=True, want_pos=True, want_raw=False):
+    """Layer-wide / per-segment selection (budget.hpp:118-158, policies.hpp:80-93, 159-196).
+
+    scores [P, N] f32 or f64 (N = seg_off[-1]); segments are ragged.
+    mode: "adaptive" (Algorithm 1), "uniform", or "given" (per-segment top-k with `budgets`).
+    Returns dict(budgets int32 [P,S], keep uint8 [P,N], kept_pos int32 [P, stride], raw int32 [P,S]).
+    """
+    _need_cuda(scores)
+    if scores.dtype not in (torch.float32, torch.float64):
+        raise L.InvalidArgument(1, "segmented_select: scores must be f32 or f64")
+    P, N = scores.shape
+    off = np.ascontiguousarray(np.asarray(seg_off, dtype=np.int64))
+    S = off.size - 1
+    if S > 0 and int(off[-1]) != N:
+        raise L.InvalidArgument(1, "segmented_select: seg_off[-1] != N")
+    dev = scores.device
+    mode_i = {"adaptive": L.ALLOC_ADAPTIVE, "uniform": L.ALLOC_UNIFORM, "given": L.ALLOC_GIVEN}[mode]
+    if budgets is None:
+        budgets = torch.empty((P, max(S, 1)), dtype=torch.int32, device=dev)
+    stride = N if (mode_i == L.ALLOC_GIVEN or totals is not None) else int(total)
+    stride = max(stride, 1)
+    keep = torch.empty((P, max(N, 1)), dtype=torch.uint8, device=dev) if want_keep else None
+    pos = torch.empty((P, stride), dtype=torch.int32, device=dev) if want_pos else None
+    raw = torch.empty((P, max(S, 1)), dtype=torch.int32, device=dev) if want_raw else None
+    cfg = L.SelectConfig(mode_i, int(bool(blend)), int(bool(repair)), int(bool(streaming)), float(alpha),
+                         int(sink_tokens))
+    lib = L.lib()
+    nbytes = C.c_size_t()
+    L.check(lib.adakv_segmented_select_workspace(P, S, C.byref(nbytes)))
+    ws = workspace(nbytes.value, dev, "select")
+    L.check(lib.adakv_segmented_select(L.F64 if scores.dtype == torch.float64 else L.F32, P, S,
+                                       off.ctypes.data_as(L.PI64), _p(scores), int(total), _p(totals),
+                                       C.byref(cfg), _p(raw), _p(budgets), _p(keep), _p(pos), stride, _p(ws),
+                                       ws.numel(), _stream()))
+    return {"budgets": budgets[:, :S], "keep": None if keep is None else keep[:, :N], "kept_pos": pos,
+            "raw": None if raw is None else raw[:, :S], "ws": ws}
+
+
+def workspace_status(ws: torch.Tensor) -> None:
+    """Raises the reference's exception if a device-side check latched an error."""
+    L.check(L.lib().adakv_workspace_status(_p(ws), _stream()))
+
+
+def decode_workspace_bytes(P, H, G, d, max_rows) -> int:
+    nbytes = C.c_size_t()
+    L.check(L.lib().adakv_decode_workspace(P, H, G, d, max_rows, C.byref(nbytes)))
+    return nbytes.value
+
+
+def decode(q: torch.Tensor, cache: CompressedCache, k_new: torch.Tensor | None = None,
+           v_new: torch.Tensor | None = None, scale=True, max_rows: int | None = None,
+           out: torch.Tensor | None = None, ws: torch.Tensor | None = None) -> torch.Tensor:
+    """One decode step over the compressed cache (attention.hpp:169-196, report.hpp:133-144),
+    with append_kv (attention.hpp:126-134) of (k_new, v_new) [P, G, d] fused in.
+
+    q [P, H, d] -> out [P, H, d].  `ws` must be zero-initialised before first use
+    (the kernel keeps its tickets re-armed), e.g. torch.zeros(decode_workspace_bytes(...)).
+    """
+    _need_cuda(q, k_new, v_new)
+    P, H, d = q.shape
+    mr = int(max_rows if max_rows is not None else cache.max_rows + 1)
+    if out is None:
+        out = torch.empty_like(q)
+    lib = L.lib()
+    if ws is None:
+        ws = workspace(decode_workspace_bytes(P, H, cache.G, d, mr), q.device, "decode")
+    L.check(lib.adakv_decode(_dt(q), P, H, cache.G, d, int(bool(scale)), _p(q), _p(cache.k), _p(cache.v),
+                             _p(cache.seg_start), _p(cache.seqlens), mr, _p(k_new), _p(v_new), _p(out), _p(ws),
+                             ws.numel(), _stream()))
+    return out
+
+
+def append_kv(cache: CompressedCache, k_new: torch.Tensor, v_new: torch.Tensor) -> None:
+    """append_kv (attention.hpp:126-134) for every segment: k_new/v_new [P*G, d]."""
+    _need_cuda(k_new, v_new)
+    L.check(L.lib().adakv_append_kv(_dt(k_new), cache.P * cache.G, cache.d, _p(cache.k), _p(cache.v),
+                                    _p(cache.seg_start), _p(cache.seqlens), _p(k_new), _p(v_new), _stream()))
+
+
+# ---------------------------------------------------------------- budget helpers (device fp64)
+def _i64(x):
+    return np.ascontiguousarray(np.asarray(x, dtype=np.int64))
+
+
+def _ptr(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def apportion(quotas, total, caps=None):
+    q = np.ascontiguousarray(np.asarray(quotas, np.float64))
+    out = np.zeros(max(q.size, 1), np.int64)
+    c = None if caps is None else _i64(caps)
+    L.check(L.lib().adakv_apportion(_ptr(q), q.size, int(total), _ptr(c), _ptr(out)))
+    return out[:q.size]
+
+
+def uniform_allocation(total, h, caps=None):
+    out = np.zeros(max(int(h), 1), np.int64)
+    c = None if caps is None else _i64(caps)
+    L.check(L.lib().adakv_uniform_allocation(int(total), int(h), _ptr(c), _ptr(out)))
+    return out[:int(h)]
+
+
+def safeguard_blend(adaptive, total, h, alpha, caps=None, adaptive_total=None):
+    a = _i64(adaptive)
+    out = np.zeros(max(int(h), 1), np.int64)
+    c = None if caps is None else _i64(caps)
+    at = total if adaptive_total is None else adaptive_total
+    L.check(L.lib().adakv_safeguard_blend(_ptr(a), int(at), int(total), int(h), float(alpha), _ptr(c), _ptr(out)))
+    return out[:int(h)]
+
+
+def repair_zero_budgets(counts, caps):
+    c = _i64(counts).copy()
+    L.check(L.lib().adakv_repair_zero_budgets(_ptr(c), _ptr(_i64(caps)), c.size))
+    return c
+
+
+def pyramid_layer_budgets(avg, layers, beta_max, beta_min):
+    out = np.zeros(max(int(layers), 1), np.int64)
+    L.check(L.lib().adakv_pyramid_layer_budgets(int(avg), int(layers), float(beta_max), float(beta_min), _ptr(out)))
+    return out[:int(layers)]

@@ -1,0 +1,97 @@
+"""Model-level driver: compress every layer after prefill, then decode over the
+compressed caches with one CUDA graph per decode step.
+
+Problems are laid out layer-major: problem index = layer * B + request.  All
+layers are compressed by ONE adakv_compress call (the prompt caches of every layer
+exist once prefill has finished -- the SnapKV/Ada-KV setting),
+which lets the per-problem selection clusters of all layers run concurrently.
+Decode keeps the model's sequential layer dependence: one adakv_decode launch
+per layer per step (fused append + split-K attention + combine), captured once
+into a CUDA graph and replayed.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib as L
+from . import ops
+
+
+def compress_model(q, k, v, layer_budget, *, kind="ada_snapkv", pool_kernel=7, alpha=0.2, sink_tokens=4,
+                   reserve=0, layer_budgets=None, out=None, ws=None) -> ops.CompressedCache:
+    """q [L, B, H, m, d]; k, v [L, B, G, n, d] -> one CompressedCache with P = L*B problems."""
+    Lyr, B = q.shape[:2]
+    qq = q.reshape(Lyr * B, *q.shape[2:])
+    kk = k.reshape(Lyr * B, *k.shape[2:])
+    vv = v.reshape(Lyr * B, *v.shape[2:])
+    return ops.compress(qq, kk, vv, layer_budget, kind=kind, pool_kernel=pool_kernel, alpha=alpha,
+                        sink_tokens=sink_tokens, reserve=reserve, layer_budgets=layer_budgets, out=out, ws=ws)
+
+
+class DecodeGraph:
+    """One decode step over all layers, captured as a CUDA graph.
+
+    Static device buffers q [L, B, H, d], k_new / v_new [L, B, G, d] and out [L, B, H, d]
+    are refreshed by the caller between replays (e.g. copy_ from pinned host memory).
+    """
+
+    def __init__(self, cache: ops.CompressedCache, layers: int, batch: int, max_rows: int, scale=True,
+                 use_graph=True):
+        self.cache = cache
+        self.L, self.B = layers, batch
+        H, G, d = cache.H, cache.G, cache.d
+        dev = cache.k.device
+        dt = cache.k.dtype
+        self.q = torch.zeros((layers, batch, H, d), dtype=dt, device=dev)
+        self.k_new = torch.zeros((layers, batch, G, d), dtype=dt, device=dev)
+        self.v_new = torch.zeros((layers, batch, G, d), dtype=dt, device=dev)
+        self.out = torch.zeros((layers, batch, H, d), dtype=dt, device=dev)
+        self.max_rows = int(max_rows)
+        nb = ops.decode_workspace_bytes(batch, H, G, d, self.max_rows)
+        self.ws = torch.zeros(nb, dtype=torch.uint8, device=dev)
+        self.scale = int(bool(scale))
+        self._dt = ops._dt(self.q)
+        self._lib = L.lib()
+        self.graph = None
+        if use_graph:
+            s = torch.cuda.Stream(device=dev)
+            s.wait_stream(torch.cuda.current_stream())
+            self.graph = torch.cuda.CUDAGraph()
+            # capture does not execute: the caches are untouched by capture itself
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(self.graph, stream=s):
+                    self._launch_all()
+            torch.cuda.current_stream().wait_stream(s)
+
+    def _launch_all(self):
+        c = self.cache
+        H, G, d, B = c.H, c.G, c.d, self.B
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        for l in range(self.L):
+            seg = l * B * G
+            L.check(self._lib.adakv_decode(
+                self._dt, B, H, G, d, self.scale, C.c_void_p(self.q[l].data_ptr()), C.c_void_p(c.k.data_ptr()),
+                C.c_void_p(c.v.data_ptr()), C.c_void_p(c.seg_start.data_ptr() + 4 * seg),
+                C.c_void_p(c.seqlens.data_ptr() + 4 * seg), self.max_rows, C.c_void_p(self.k_new[l].data_ptr()),
+                C.c_void_p(self.v_new[l].data_ptr()), C.c_void_p(self.out[l].data_ptr()),
+                C.c_void_p(self.ws.data_ptr()), self.ws.numel(), st))
+
+    def step(self):
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._launch_all()
+        return self.out
+
+
+def algorithmic_bytes_compress(L, B, H, G, n_o, m, d, layer_budget, esize=2):
+    """e*(G*n_o*d + H*m*d) + 4*e*d*LB per layer per request."""
+    return L * B * (esize * (G * n_o * d + H * m * d) + 4 * esize * d * layer_budget)
+
+
+def algorithmic_bytes_decode_step(L, B, H, G, d, total_rows, esize=2):
+    """2*e*d*sum_g len_g + 2*e*H*d + 2*e*G*d per step per layer per request;
+    total_rows = sum over all layers/requests/groups of the cache length attended this step."""
+    return 2 * esize * d * total_rows + L * B * (2 * esize * H * d + 2 * esize * G * d)

@@ -1,0 +1,352 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Gates (BASELINE.json north_star):
+  * budgets, keep masks and kept positions BIT-EXACT when fed identical scores;
+  * retained K/V rows are exact copies;
+  * scores and decode outputs within stated tolerances:
+      fp64 path  : |d| <= 1e-12 * max_j s_gj      (exp() ulps + sum order only)
+      fp32 path  : |d| <= 1e-5 * max_j s_gj
+      bf16 inputs: scores vs the oracle on the SAME bf16 values upcast to fp64,
+                   |d| <= 1e-4 * max_j s_gj (fp32 accumulation); decode outputs
+                   max-abs <= 2e-2 and <= 1e-2 * max|o| (bf16 output rounding).
+"""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2407_11550_b200 as A  # noqa: E402
+from paper_2407_11550_b200.synthetic import planted_layer  # noqa: E402
+
+
+def T(x, dtype, dev):
+    return torch.as_tensor(np.ascontiguousarray(x)).to(device=dev, dtype=dtype)
+
+
+# --------------------------------------------------------------------------- budget helpers
+def test_budget_helpers_bit_exact(dev, oracle_mod):
+    O = oracle_mod
+    assert A.safeguard_blend([9, 1], 10, 2, 0.2).tolist() == [6, 4]          # budget_test.cpp:170-174
+    assert A.uniform_allocation(10, 3).tolist() == [4, 3, 3]                  # budget_test.cpp:45-48
+    assert A.pyramid_layer_budgets(100, 3, 1.5, 0.5).tolist() == [150, 100, 50]
+    assert A.apportion([3.5, 3.5, 3.0], 8, [10, 10, 10]).tolist() == [3, 3, 2]
+    rng = np.random.default_rng(1)
+    for _ in range(150):
+        h = int(rng.integers(1, 9))
+        caps = rng.integers(1, 40, size=h)
+        total = int(rng.integers(0, caps.sum() + 1))
+        assert np.array_equal(A.uniform_allocation(total, h, caps), O.uniform_allocation(total, h, caps))
+        counts = rng.integers(0, 30, size=h)
+        t = int(counts.sum())
+        alpha = float(rng.random())
+        assert np.array_equal(A.safeguard_blend(counts, t, h, alpha), O.safeguard_blend(counts, t, h, alpha))
+        q = rng.random(h) * 10
+        tot = int(rng.integers(0, 40))
+        assert np.array_equal(A.apportion(q, tot), O.apportion(q, tot))
+        layers = int(rng.integers(1, 33))
+        avg = int(rng.integers(1, 4096))
+        bmin = 0.1 + 0.9 * float(rng.random())
+        bmax = bmin + 2.0 * float(rng.random())
+        assert np.array_equal(A.pyramid_layer_budgets(avg, layers, bmax, bmin),
+                              O.pyramid_layer_budgets(avg, layers, bmax, bmin))
+        z = counts.copy()
+        z[rng.integers(0, h)] = 0
+        if z.sum() >= h:
+            assert np.array_equal(A.repair_zero_budgets(z, np.full(h, 100)), O.repair_zero_budgets(z, np.full(h, 100)))
+    with pytest.raises(A.InvalidArgument):
+        A.uniform_allocation(3, 2, [1, 1])
+
+
+# --------------------------------------------------------------------------- selection
+def _oracle_select(O, s64, total, alpha, blend=True, repair=True):
+    G, n = s64.shape
+    raw = O.adaptive_allocation(list(s64), total)
+    b = O.safeguard_blend(raw, total, G, alpha, np.full(G, n)) if blend else raw
+    if repair:
+        b = O.repair_zero_budgets(b, np.full(G, n))
+    keep = np.stack([O.topk_decision(s64[i], int(b[i])) for i in range(G)])
+    return raw, b, keep
+
+
+def _kept_pos(keep):
+    return np.concatenate([np.nonzero(row)[0] for row in keep]).astype(np.int32)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_select_golden_config1(dev, oracle_mod, dtype):
+    """Reference generator config 1: identical scores -> identical budgets/decisions."""
+    O = oracle_mod
+    z = load_golden("config1.npz")
+    scores = z["scores"]
+    h, gqa, n, d_h, window, seed, LB = z["meta"].tolist()
+    G = h // gqa
+    outside = LB - window * G
+    s = T(scores, dtype, dev).reshape(1, G * n)
+    r = A.segmented_select(s, np.arange(G + 1) * n, outside, "adaptive", blend=True, alpha=0.2, repair=True,
+                           want_raw=True)
+    s64 = s.double().cpu().numpy().reshape(G, n)
+    raw, b, keep = _oracle_select(O, s64, outside, 0.2)
+    if dtype == torch.float64:
+        assert b.tolist() == z["alloc"].tolist() == [837, 837, 1454, 837, 837, 837, 1460, 837]
+        assert np.array_equal(keep, z["keep"])
+    assert r["raw"][0].cpu().tolist() == raw.tolist()
+    assert r["budgets"][0].cpu().tolist() == b.tolist()
+    assert np.array_equal(r["keep"][0].cpu().numpy().reshape(G, n), keep)
+    assert np.array_equal(r["kept_pos"][0, :outside].cpu().numpy(), _kept_pos(keep))
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_select_adversarial_ties(dev, oracle_mod, dtype):
+    """All-equal, quantised k/64 and underflowed-zero scores (tie-break = lowest flat index)."""
+    O = oracle_mod
+    z = load_golden("select_ties.npz")
+    for name in ("equal", "quantised", "underflow", "random"):
+        s64 = z[f"{name}_scores"]
+        G, n = s64.shape
+        s = T(s64, dtype, dev).reshape(1, -1)
+        s64 = s.double().cpu().numpy().reshape(G, n)
+        off = np.arange(G + 1) * n
+        for k in (0, 1, 17, 400, 1203, G * n):
+            r = A.segmented_select(s, off, k, "adaptive", want_raw=True)
+            raw = O.adaptive_allocation(list(s64), k)
+            if dtype == torch.float64:
+                assert np.array_equal(raw, z[f"{name}_{k}_raw"])
+            assert r["budgets"][0].cpu().tolist() == raw.tolist(), (name, k)
+            keep = np.stack([O.topk_decision(s64[i], int(raw[i])) for i in range(G)])
+            assert np.array_equal(r["keep"][0].cpu().numpy().reshape(G, n), keep), (name, k)
+            for alpha in (0.0, 0.2, 1.0):
+                rb = A.segmented_select(s, off, k, "adaptive", blend=True, alpha=alpha)
+                assert rb["budgets"][0].cpu().tolist() == O.safeguard_blend(raw, k, G, alpha, np.full(G, n)).tolist()
+        ks = z[f"{name}_topk_k"]
+        rg = A.segmented_select(s, off, 0, "given", budgets=T(ks[None, :], torch.int32, dev))
+        exp = np.stack([O.topk_decision(s64[i], int(ks[i])) for i in range(G)])
+        assert np.array_equal(rg["keep"][0].cpu().numpy().reshape(G, n), exp), name
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_select_ragged_evict_rows(dev, oracle_mod, dtype):
+    """evict_rows (policies.hpp:298-323) over ragged heads, several problems per launch."""
+    O = oracle_mod
+    rng = np.random.default_rng(11)
+    for trial in range(12):
+        S = int(rng.integers(1, 12))
+        lens = rng.integers(1, 3000, size=S)
+        off = np.concatenate([[0], np.cumsum(lens)])
+        P = int(rng.integers(1, 4))
+        rows64 = rng.exponential(size=(P, int(off[-1])))
+        if trial % 3 == 0:
+            rows64 = np.round(rows64 * 8) / 8  # heavy ties
+        s = T(rows64, dtype, dev)
+        s64 = s.double().cpu().numpy()
+        total = int(rng.integers(S, int(off[-1]) + 1))
+        alpha = float(rng.random())
+        for adaptive in (True, False):
+            r = A.segmented_select(s, off, total, "adaptive" if adaptive else "uniform", blend=adaptive,
+                                   alpha=alpha, repair=True)
+            for p in range(P):
+                rows = [s64[p, off[i]:off[i + 1]] for i in range(S)]
+                alloc, keep = O.evict_rows(rows, total, adaptive, alpha)
+                assert r["budgets"][p].cpu().tolist() == alloc.tolist()
+                assert np.array_equal(r["keep"][p].cpu().numpy(), np.concatenate(keep))
+                kp = np.concatenate([np.nonzero(x)[0] for x in keep])
+                assert np.array_equal(r["kept_pos"][p, :total].cpu().numpy(), kp)
+
+
+def test_select_streaming(dev, oracle_mod):
+    O = oracle_mod
+    s = torch.rand(2, 8 * 100, device=dev, dtype=torch.float32)
+    off = np.arange(9) * 100
+    r = A.segmented_select(s, off, 200, "uniform", repair=True, streaming=True, sink_tokens=4)
+    b = O.uniform_allocation(200, 8, np.full(8, 100))
+    exp = np.concatenate([O.streaming_llm_decision(100, min(4, int(x)), int(x) - min(4, int(x))) for x in b])
+    for p in range(2):
+        assert np.array_equal(r["keep"][p].cpu().numpy(), exp)
+
+
+# --------------------------------------------------------------------------- scoring
+def _split_case(z, i):
+    p = f"c{i}_"
+    return (z[p + "q"], z[p + "k_out"], z[p + "v_out"], z[p + "k_win"], z[p + "v_win"], z[p + "params"].tolist(),
+            float(z[p + "alpha"]))
+
+
+def _kv(ko, kw):
+    return np.concatenate([ko, kw], axis=1)[None]
+
+
+def test_window_scores_fp64_vs_oracle(dev, oracle_mod):
+    O = oracle_mod
+    z = load_golden("evict_small.npz")
+    for i in range(0, int(z["count"]), 5):
+        q, ko, vo, kw, vw, (LB, pk, kind), alpha = _split_case(z, i)
+        H, m, d = q.shape
+        G, n, _ = ko.shape
+        gs, hs = A.window_scores(T(q[None], torch.float64, dev), T(_kv(ko, kw), torch.float64, dev), pk,
+                                 head_scores=True)
+        ref = z[f"c{i}_group_scores"].reshape(G, n)
+        tol = 1e-12 * np.abs(ref).max(axis=1, keepdims=True)
+        assert np.all(np.abs(gs[0].cpu().numpy() - ref) <= tol), i
+        for h in range(H):
+            rh = O.window_scores(q[h], ko[h // (H // G)], pk)
+            assert np.allclose(hs[0, h].cpu().numpy(), rh, rtol=1e-12, atol=1e-300)
+
+
+@pytest.mark.parametrize("dtype,rel", [(torch.float32, 1e-5), (torch.bfloat16, 1e-4)])
+def test_window_scores_llama_shape(dev, oracle_mod, dtype, rel):
+    """Config-1 shape (32 Q / 8 KV heads, d=128, m=32, k=7, 4K prompt), planted heads."""
+    O = oracle_mod
+    q, k, v = planted_layer(1, 32, 8, 4064, 32, 128, seed=7, dtype=dtype, device=dev)
+    gs = A.window_scores(q, k, 7)
+    q64 = q.double().cpu().numpy()[0]
+    k64 = k.double().cpu().numpy()[0]
+    for g in (0, 3, 7):  # oracle cost: ~1 s per group
+        per = [O.window_scores(q64[h], k64[g, :4064], 7) for h in range(g * 4, g * 4 + 4)]
+        ref = O.group_mean_scores(np.stack(per), 4)[0]
+        err = np.abs(gs[0, g].double().cpu().numpy() - ref).max()
+        assert err <= rel * ref.max(), (g, err, ref.max())
+
+
+# --------------------------------------------------------------------------- compress (evict_layer)
+def test_compress_fp64_golden(dev, oracle_mod):
+    """All 60 reference-generated evict_layer cases (5 kinds) through the full device pipeline."""
+    O = oracle_mod
+    z = load_golden("evict_small.npz")
+    kinds = {v: k for k, v in O.KINDS.items()}
+    for i in range(int(z["count"])):
+        q, ko, vo, kw, vw, (LB, pk, kind), alpha = _split_case(z, i)
+        H, m, d = q.shape
+        G, n, _ = ko.shape
+        out = A.compress(T(q[None], torch.float64, dev), T(_kv(ko, kw), torch.float64, dev),
+                         T(_kv(vo, vw), torch.float64, dev), LB, kind=kinds[kind], pool_kernel=pk, alpha=alpha,
+                         return_scores=True, return_keep=True)
+        ref_scores = z[f"c{i}_group_scores"].reshape(G, n)
+        assert np.all(np.abs(out.scores[0].cpu().numpy() - ref_scores) <= 1e-12 * np.abs(ref_scores).max()), i
+        # identical-score gate: the oracle's selection on the GPU's scores == GPU selection
+        r = O.evict_layer(q, ko, vo, kw, vw, LB, kind=kinds[kind], pool_kernel=pk, alpha=alpha)
+        assert out.budgets.cpu().tolist() == z[f"c{i}_alloc"].tolist() == r.alloc.tolist(), i
+        assert np.array_equal(out.keep[0].cpu().numpy().ravel(), z[f"c{i}_keep"]), i
+        assert out.seqlens.cpu().tolist() == z[f"c{i}_ret_len"].tolist()
+        rows = torch.cat([out.segment(0, g)[0] for g in range(G)]).cpu().numpy()
+        vals = torch.cat([out.segment(0, g)[1] for g in range(G)]).cpu().numpy()
+        assert np.array_equal(rows, z[f"c{i}_k_ret"]) and np.array_equal(vals, z[f"c{i}_v_ret"]), i
+
+
+@pytest.mark.parametrize("kind", ["ada_snapkv", "snapkv", "streaming_llm"])
+def test_compress_bf16_llama_identical_scores(dev, oracle_mod, kind):
+    """bf16 Llama-shaped layers (P=2): GPU scores within tolerance of the oracle; the oracle's
+    selection fed the GPU's own scores reproduces budgets, decisions and the packed rows bit-exactly."""
+    O = oracle_mod
+    P, H, G, m, n_o, d = 2, 32, 8, 32, 4064, 128
+    LB = 1024 * G
+    q, k, v = planted_layer(P, H, G, n_o, m, d, seed=3, dtype=torch.bfloat16, device=dev)
+    out = A.compress(q, k, v, LB, kind=kind, pool_kernel=7, alpha=0.2, reserve=16, return_scores=True,
+                     return_keep=True)
+    torch.cuda.synchronize()
+    outside = LB - m * G
+    for p in range(P):
+        s64 = out.scores[p].double().cpu().numpy()
+        if kind == "ada_snapkv":
+            raw, b, keep = _oracle_select(O, s64, outside, 0.2)
+        else:
+            b = O.repair_zero_budgets(O.uniform_allocation(outside, G, np.full(G, n_o)), np.full(G, n_o))
+            if kind == "snapkv":
+                keep = np.stack([O.topk_decision(s64[i], int(b[i])) for i in range(G)])
+            else:
+                keep = np.stack([O.streaming_llm_decision(n_o, min(4, int(x)), int(x) - min(4, int(x))) for x in b])
+        assert out.budgets[p * G:(p + 1) * G].cpu().tolist() == b.tolist()
+        assert np.array_equal(out.keep[p].cpu().numpy(), keep)
+        kk = k[p].cpu()
+        vv = v[p].cpu()
+        for g in range(G):
+            idx = np.concatenate([np.nonzero(keep[g])[0], n_o + np.arange(m)])
+            kr, vr = out.segment(p, g)
+            assert torch.equal(kr.cpu(), kk[g, idx]) and torch.equal(vr.cpu(), vv[g, idx])
+    # scores vs the oracle on the same bf16 values (one group per problem; ~1 s each)
+    q64, k64 = q.double().cpu().numpy(), k.double().cpu().numpy()
+    for p in range(P):
+        g = 5
+        per = [O.window_scores(q64[p, h], k64[p, g, :n_o], 7) for h in range(g * 4, g * 4 + 4)]
+        ref = O.group_mean_scores(np.stack(per), 4)[0]
+        assert np.abs(out.scores[p, g].double().cpu().numpy() - ref).max() <= 1e-4 * ref.max()
+
+
+def test_compress_per_problem_budgets(dev, oracle_mod):
+    """pyramid schedule (budget.hpp:169-191): per-problem layer budgets in one launch."""
+    O = oracle_mod
+    P, H, G, m, n_o, d = 4, 8, 2, 4, 300, 16
+    q, k, v = planted_layer(P, H, G, n_o, m, d, seed=5, dtype=torch.float32, device=dev)
+    lbs = A.pyramid_layer_budgets(200, P, 1.5, 0.5) + m * G
+    out = A.compress(q, k, v, 0, kind="ada_pyramid", layer_budgets=torch.tensor(lbs, device=dev),
+                     return_scores=True, return_keep=True, reserve=3)
+    for p in range(P):
+        s64 = out.scores[p].double().cpu().numpy()
+        raw, b, keep = _oracle_select(O, s64, int(lbs[p]) - m * G, 0.2)
+        assert out.budgets[p * G:(p + 1) * G].cpu().tolist() == b.tolist()
+        assert np.array_equal(out.keep[p].cpu().numpy(), keep)
+    starts = out.seg_start.cpu().numpy()
+    assert starts[0] == 0 and np.all(np.diff(starts) > 0)
+
+
+# --------------------------------------------------------------------------- decode
+def _cache_from_oracle(O, dev, dtype, rng, G=2, H=8, d=16, m=3, n=50, LB=40, reserve=4):
+    q = rng.normal(size=(H, m, d))
+    ko, vo = rng.normal(size=(G, n, d)), rng.normal(size=(G, n, d))
+    kw, vw = rng.normal(size=(G, m, d)), rng.normal(size=(G, m, d))
+    out = A.compress(T(q[None], dtype, dev), T(_kv(ko, kw), dtype, dev), T(_kv(vo, vw), dtype, dev), LB,
+                     kind="ada_snapkv", pool_kernel=3, reserve=reserve)
+    return out
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_decode_multistep_append_vs_oracle(dev, oracle_mod, dtype):
+    O = oracle_mod
+    rng = np.random.default_rng(4)
+    G, H, d = 2, 8, 16
+    cache = _cache_from_oracle(O, dev, dtype, rng, G=G, H=H, d=d)
+    ws = torch.zeros(A.ops.decode_workspace_bytes(1, H, G, d, cache.max_rows + 8), dtype=torch.uint8, device=dev)
+    segs = [[x.double().cpu().numpy() for x in cache.segment(0, g)] for g in range(G)]
+    for step in range(4):
+        qd = rng.normal(size=(H, d))
+        kn, vn = rng.normal(size=(G, d)), rng.normal(size=(G, d))
+        o = A.decode(T(qd[None], dtype, dev), cache, T(kn[None], dtype, dev), T(vn[None], dtype, dev),
+                     max_rows=cache.max_rows + 8, ws=ws)
+        for g in range(G):  # append_kv: the new row goes last (attention.hpp:126-134)
+            segs[g][0] = np.vstack([segs[g][0], kn[g]])
+            segs[g][1] = np.vstack([segs[g][1], vn[g]])
+        off = np.concatenate([[0], np.cumsum([s[0].shape[0] for s in segs])])
+        ref = O.decode_attention(qd, np.vstack([s[0] for s in segs]), np.vstack([s[1] for s in segs]), off)
+        tol = 1e-12 if dtype == torch.float64 else 2e-5
+        assert np.abs(o[0].double().cpu().numpy() - ref).max() <= tol * max(1.0, np.abs(ref).max())
+        assert cache.seqlens.cpu().tolist() == [s[0].shape[0] for s in segs]
+        for g in range(G):
+            kr, vr = cache.segment(0, g)
+            assert np.array_equal(kr.double().cpu().numpy(), segs[g][0])
+
+
+def test_decode_bf16_llama_shape(dev, oracle_mod):
+    O = oracle_mod
+    P, H, G, m, n_o, d = 2, 32, 8, 32, 4064, 128
+    q, k, v = planted_layer(P, H, G, n_o, m, d, seed=9, dtype=torch.bfloat16, device=dev)
+    cache = A.compress(q, k, v, 1024 * G, reserve=8)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(0)
+    qd = torch.randn((P, H, d), generator=gen, device=dev).to(torch.bfloat16)
+    o = A.decode(qd, cache)
+    for p in range(P):
+        segs = [cache.segment(p, g) for g in range(G)]
+        off = np.concatenate([[0], np.cumsum([s[0].shape[0] for s in segs])])
+        ref = O.decode_attention(qd[p].double().cpu().numpy(), torch.cat([s[0] for s in segs]).double().cpu().numpy(),
+                                 torch.cat([s[1] for s in segs]).double().cpu().numpy(), off)
+        err = np.abs(o[p].double().cpu().numpy() - ref).max()
+        assert err <= 2e-2 and err <= 1e-2 * max(np.abs(ref).max(), 1e-3) + 4e-3, err
+
+
+def test_device_error_latch(dev):
+    """topk_decision k > n (policies.hpp:83) detected on the device -> InvalidArgument."""
+    s = torch.rand(1, 10, device=dev)
+    r = A.segmented_select(s, [0, 5, 10], 0, "given", budgets=torch.tensor([[6, 1]], dtype=torch.int32, device=dev))
+    with pytest.raises(A.InvalidArgument):
+        A.workspace_status(r["ws"])
