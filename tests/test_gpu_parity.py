@@ -311,6 +311,9 @@ def test_decode_multistep_append_vs_oracle(dev, oracle_mod, dtype):
     for step in range(4):
         qd = rng.normal(size=(H, d))
         kn, vn = rng.normal(size=(G, d)), rng.normal(size=(G, d))
+        kn = torch.as_tensor(kn).to(dtype).double().numpy()  # the cache stores `dtype`
+        vn = torch.as_tensor(vn).to(dtype).double().numpy()
+        qd = torch.as_tensor(qd).to(dtype).double().numpy()
         o = A.decode(T(qd[None], dtype, dev), cache, T(kn[None], dtype, dev), T(vn[None], dtype, dev),
                      max_rows=cache.max_rows + 8, ws=ws)
         for g in range(G):  # append_kv: the new row goes last (attention.hpp:126-134)
