@@ -96,6 +96,10 @@ typedef struct adakv_layer_shape {
 
 const char* adakv_last_error(void);
 int adakv_abi_version(void);
+/* Selects the scoring kernel for eligible shapes (bf16, d == 128, m == 32, g*m <= 128):
+ * 1 = tcgen05 tensor-core kernel (default), 0 = the generic SIMT kernel.  Returns the
+ * previous setting.  Both compute the same function; this exists for A/B checks. */
+int adakv_set_tensor_core_scoring(int enabled);
 /* Reads back (synchronously) the device error word latched in a workspace. */
 adakv_status adakv_workspace_status(const void* workspace, adakv_stream_t stream);
 

@@ -67,6 +67,8 @@ def _sig(L):
     S = C.c_int
     L.adakv_last_error.restype = C.c_char_p
     L.adakv_abi_version.restype = C.c_int
+    L.adakv_set_tensor_core_scoring.argtypes = [C.c_int]
+    L.adakv_set_tensor_core_scoring.restype = C.c_int
     L.adakv_workspace_status.argtypes = [VP, VP]
     L.adakv_compress.argtypes = [S, C.POINTER(LayerShape), C.POINTER(PolicyConfig), I64, VP, VP, VP, VP, I64,
                                  VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP]
@@ -87,8 +89,6 @@ def _sig(L):
     L.adakv_safeguard_blend.argtypes = [VP, I64, I64, I64, C.c_double, VP, VP]
     L.adakv_repair_zero_budgets.argtypes = [VP, VP, I64]
     L.adakv_pyramid_layer_budgets.argtypes = [I64, I64, C.c_double, C.c_double, VP]
-    for name in dir(L):
-        pass
     return L
 
 

@@ -2,6 +2,8 @@
 // mirroring the reference's throw sites, workspace carving, stream-ordered launches.
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -110,12 +112,16 @@ adakv_status validate_shape(const adakv_layer_shape* s) {
 
 size_t acc_size(adakv_dtype dt) { return dt == ADAKV_F64 ? 8 : 4; }
 
+std::atomic<int> g_tc_enabled{-1};  // -1: from ADAKV_DISABLE_TC at first use
+
 bool use_tc(adakv_dtype dt, const adakv_layer_shape& s, int64_t pool_kernel) {
-    static const bool disabled = [] {
+    int en = g_tc_enabled.load();
+    if (en < 0) {
         const char* e = std::getenv("ADAKV_DISABLE_TC");
-        return e && e[0] == '1';
-    }();
-    return !disabled && score_window_tc_supported(dt, s, pool_kernel);
+        en = (e && e[0] == '1') ? 0 : 1;
+        g_tc_enabled.store(en);
+    }
+    return en && score_window_tc_supported(dt, s, pool_kernel);
 }
 
 size_t score_ws(adakv_dtype dt, const adakv_layer_shape& s, int64_t pool_kernel) {
@@ -217,6 +223,11 @@ extern "C" {
 
 const char* adakv_last_error(void) { return g_last_error.c_str(); }
 int adakv_abi_version(void) { return ADAKV_B200_ABI_VERSION; }
+
+int adakv_set_tensor_core_scoring(int enabled) {
+    const int prev = g_tc_enabled.exchange(enabled ? 1 : 0);
+    return prev;
+}
 
 adakv_status adakv_workspace_status(const void* workspace, adakv_stream_t stream) {
     uint32_t e = 0;
