@@ -15,6 +15,8 @@
 // finish (atomic ticket) merges them, writes out[p, h, :], bumps seqlens and
 // re-arms the ticket -- one launch per decode step, graph-capturable (the grid is
 // sized from max_rows, so lengths can grow on the device between replays).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace adakv_b200 {
@@ -129,12 +131,14 @@ decode_kernel(const T* __restrict__ q, T* __restrict__ k_cache, T* __restrict__ 
             part_ml[slot * 2 + 1] = Ls;
         }
     }
-    __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = atomicAdd(&tickets[pg], 1u) == uint32_t(nsplit - 1);
+    if (threadIdx.x == 0) {  // one fence + ticket per CTA (grid-sync pattern)
+        __threadfence();
+        s_last = atomicAdd(&tickets[pg], 1u) == uint32_t(nsplit - 1);
+        if (s_last) __threadfence();
+    }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     for (int64_t i = tid; i < gs * d; i += kDecThreads) {
         const int64_t h = i / d, c = i % d;
         A M = -INFINITY;
@@ -201,23 +205,32 @@ adakv_status launch_t(int64_t P, int64_t H, int64_t G, int64_t d, int32_t scale,
 }  // namespace
 
 void decode_plan(int64_t P, int64_t G, int64_t max_rows, int64_t* chunk, int64_t* nsplit) {
-    // Aim for >= 2 waves of CTAs over 148 SMs, chunks of at least 64 rows.
+    // ~1.5 CTAs per SM over the P*G segments; chunks of >= 128 rows (multiples of 64,
+    // 16-row blocks x 4 warps); at most 64 splits per segment (the combine's fan-in).
     const int64_t sms = device_sm_count();
-    const int64_t target_ctas = 2 * sms;
     const int64_t segs = P * G > 0 ? P * G : 1;
-    int64_t want_splits = ceil_div(target_ctas, segs);
-    int64_t c = ceil_div(max_rows > 0 ? max_rows : 1, want_splits);
-    c = ((c + 31) / 32) * 32;
-    if (c < 64) c = 64;
+    const int64_t rows = max_rows > 0 ? max_rows : 1;
+    const int64_t want_splits = std::max<int64_t>(1, (3 * sms / 2 + segs - 1) / segs);
+    int64_t c = ceil_div(rows, want_splits);
+    c = std::max<int64_t>(128, ((c + 63) / 64) * 64);
+    c = std::max<int64_t>(c, ((ceil_div(rows, 64) + 63) / 64) * 64);
     *chunk = c;
-    *nsplit = ceil_div(max_rows > 0 ? max_rows : 1, c);
+    *nsplit = ceil_div(rows, c);
 }
+
+size_t decode_tc_workspace(int64_t P, int64_t H, int64_t G, int64_t d);
 
 size_t decode_workspace_bytes(int64_t P, int64_t H, int64_t G, int64_t d, int64_t max_rows, size_t acc) {
     int64_t chunk, nsplit;
     decode_plan(P, G, max_rows, &chunk, &nsplit);
-    return 3 * 256 + size_t(P * G) * 4 + size_t(P * G * nsplit * (H / G)) * (2 + d) * acc;
+    return std::max<size_t>(3 * 256 + size_t(P * G) * 4 + size_t(P * G * nsplit * (H / G)) * (2 + d) * acc,
+                            decode_tc_workspace(P, H, G, d));
 }
+
+bool decode_tc_supported(adakv_dtype dt, int64_t H, int64_t G, int64_t d, int64_t nsplit);
+adakv_status launch_decode_tc(int64_t P, int64_t H, int64_t G, int32_t scale, const void* q, void* kc, void* vc,
+                              const int32_t* ss, int32_t* sl, const void* kn, const void* vn, void* out, void* ws,
+                              cudaStream_t stream);
 
 adakv_status launch_decode(adakv_dtype dt, int64_t P, int64_t H, int64_t G, int64_t d, int32_t scale,
                            const void* q, void* kc, void* vc, const int32_t* ss, int32_t* sl,
@@ -225,6 +238,8 @@ adakv_status launch_decode(adakv_dtype dt, int64_t P, int64_t H, int64_t G, int6
                            cudaStream_t stream) {
     int64_t chunk, nsplit;
     decode_plan(P, G, max_rows, &chunk, &nsplit);
+    if (decode_tc_supported(dt, H, G, d, nsplit))
+        return launch_decode_tc(P, H, G, scale, q, kc, vc, ss, sl, kn, vn, out, ws, stream);
     if (H / G > kMaxGroupHeads) return fail(ADAKV_UNSUPPORTED, "decode: more than 16 query heads per KV group");
     if (d > 256) return fail(ADAKV_UNSUPPORTED, "decode: head_dim > 256");
     const int J = int(ceil_div(d, 32));

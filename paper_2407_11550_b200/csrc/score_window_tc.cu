@@ -1,34 +1,34 @@
 // score_window_tc.cu -- K1 on the 5th-generation tensor cores (bf16, d == 128, m == 32,
-// g*m <= 128): observation-window scoring fused into two persistent passes.
+// g*m <= 128): observation-window scoring in two persistent passes.
 //
-// Reference semantics (see score_window.cu for the file:line list): per KV group, the
-// g*m window rows (g heads x m rows) are softmaxed over the OUTSIDE keys, max-pooled
-// along keys (k odd, stride 1, padded cells excluded), averaged over rows (/m) and
-// heads (/g).
+// Reference semantics (file:line list in score_window.cu): per KV group, the g*m window
+// rows (g heads x m rows) are softmaxed over the OUTSIDE keys, max-pooled along keys
+// (k odd, stride 1, padded cells excluded), averaged over rows (/m) and heads (/g).
 //
-// B200 mapping.  The g*m <= 128 query rows of a KV group are exactly one UMMA M=128
-// tile; each 128-key K tile is the N=128 operand; d = 128 is the K extent (8 MMAs of
-// K=16).  Per CTA (1 per SM, persistent over (group, key-chunk) items):
-//   warp 0        TMA producer: Q tile (per item, double-buffered) and a 4-stage ring of
-//                 K tiles, 128B-swizzled [128 x 64] halves, 3-D tensor maps so rows
-//                 outside a group are zero-filled by the hardware;
-//   warp 1        TMEM owner + single-thread tcgen05.mma issuer, fp32 accumulators in
-//                 TMEM (2 x 128 columns, double-buffered);
-//   warps 2..5    epilogue: thread r <-> TMEM lane r <-> window row r; with m == 32 each
-//                 warp is exactly one query head.
-// Pass 1 (row statistics): online max / sum of exp2 over the tile's logits, per item a
-//   partial (max, sum) per row; the last CTA of a group (atomic ticket) folds them into
-//   (M_r, Lw_r = M_r + log2(S_r * m)).
-// Pass 2 (scores): tiles advance by 128 - 2*pad keys so every output key has its full
-//   pooling halo inside the tile; pooling is done on LOGITS in registers (exp2 is
-//   monotone), e = exp2(pool*c - Lw_r) = pooled_prob / m, then a 32-lane butterfly
-//   reduce-scatter sums the warp's 32 rows (= its head) per key in fp32, heads are summed
-//   through shared memory and divided by g.
-// The two passes run back to back over a slice of problems small enough (~48 MB of K) to
-// stay resident in the 126 MB L2, so pass 2 re-reads K from L2, not HBM (pass 1 loads
-// with evict_last, pass 2 with evict_first).
+// B200 mapping.  The g*m <= 128 query rows of a KV group are one UMMA M=128 tile; each
+// 128-key K tile is the N=128 operand; d = 128 is the K extent (8 MMAs of K=16).  One CTA
+// per SM, persistent over balanced (group, key-chunk) items, 18 warps:
+//   warp 0      TMA producer: the group's Q tile and a 3-stage ring of K tiles (128B-
+//               swizzled [128 x 64] halves; 3-D tensor maps zero-fill rows outside a group);
+//   warp 1      TMEM owner + single-thread tcgen05.mma issuer;
+//   warps 2..17 epilogue, four warps per scheduler: warp (quarter q, group c) owns TMEM lanes
+//               32q..32q+31 (= window rows, i.e. head q since m == 32) and columns 32c..32c+31.
+// Pass 1 (row statistics): online max / sum of exp2 of the fp32 logits; per item a
+//   partial (max, sum) per (row, column group); the last CTA of a group (atomic ticket)
+//   folds them into Lw_r = M_r + log2(S_r * m).
+// Pass 2 (scores): tiles advance by 128 - 2*pad keys so each output key's pooling halo is
+//   inside the tile; pooling is done on LOGITS in registers (exp2 monotone), then
+//   E = exp2(pool*c - Lw_r + 16) = 2^16 * pooled_prob / m is written as fp16 into an
+//   MN-major shared tile and the per-head row sums are a second tcgen05 MMA:
+//   D2[key][head] = E^T[key][row] * Hd[row][head] (Hd = head indicator), fp32 accumulate in
+//   TMEM.  Scores = D2 * 2^-16, group score = sum over heads / g.
+// Both passes run back to back per slice of problems small enough (~48 MB of K) to stay
+// L2-resident, so pass 2 re-reads K from L2 (pass 1 loads evict_last, pass 2 evict_first).
 #include <cuda.h>
+#include <cuda_fp16.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -40,82 +40,141 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kThreads = 192;
-constexpr int kStages = 4;
+constexpr int kEpiWarps = 16;  // 4 per scheduler; warp = (lane quarter, 32-column group)
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kStages = 3;
 constexpr int kTile = 128;
-constexpr uint32_t kTmemCols = 256;
-constexpr uint32_t kHalfBytes = 128 * 128;  // [128 rows][64 bf16]
-constexpr uint32_t kTileBytes = 2 * kHalfBytes;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kD2Col = 256;
+constexpr uint32_t kHalfBytes = 128 * 128;        // [128 rows][64 bf16]
+constexpr uint32_t kTileBytes = 2 * kHalfBytes;   // a [128 x 128] bf16 tile
+constexpr uint32_t kA2Bytes = 128 * 128 * 2;      // E^T tile, fp16
+constexpr float kEScaleLog2 = 16.f;               // E carries a 2^16 scale (fp16 range)
 
 struct __align__(1024) Smem {
-    uint8_t q[2][2][kHalfBytes];
+    uint8_t q[2][kHalfBytes];
     uint8_t k[kStages][2][kHalfBytes];
-    float head_part[2][4][kTile];
+    uint8_t a2[2][kA2Bytes];
+    uint8_t b2[2][16 * 128];
     uint64_t full[kStages], empty[kStages];
-    uint64_t q_full[2], q_empty[2];
+    uint64_t q_full, q_empty;
     uint64_t acc_full[2], acc_empty[2];
+    uint64_t e_full[2], e_empty[2];
+    uint64_t d2_full[2], d2_empty[2];
     uint32_t tmem_base;
     uint32_t is_last;
 };
+
+__device__ __forceinline__ uint64_t gtime() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct TcParams {
     int pass;
     int G, H, gs, m, n_o, step, pad;
     int tiles_per_pg, tiles_per_item, chunks_per_pg, n_items;
-    int pg_base;  // first problem*group of this slice (for outputs / stats)
+    int pg_base;
+    int debug;  // bit 1: MUFU only (no polynomial exp2); bit 2: skip the pass-1 ticket/fold
     float scale_log2;
     float log2_m;
     float inv_g;
-    float* partial;      // [pg][chunk][128][2]
-    float* final_stats;  // [pg][128][2]
+    float* partial;      // pass 1: [pg][chunk][column group][128][2]
+    float* final_stats;  // [pg][128][2]: (M_r, Lw_r)
     unsigned* tickets;   // [pg]
     float* head_scores;  // [P][H][n_o] or null
     float* group_scores; // [P][G][n_o]
 };
 
 // ------------------------------------------------------------------ epilogue helpers
-template <int BASE, int NV>
-__device__ __forceinline__ float butterfly32(float (&e)[NV], int lane) {
-    // reduce-scatter over the 32 lanes: afterwards lane l holds sum_lanes e[BASE + l]
+// exp2 of x[off .. off+count) in place; of every 8 elements, POLY go through the FMA-pipe
+// polynomial (exp2_poly2), the rest through MUFU.EX2.
+template <int N, int POLY>
+__device__ __forceinline__ void exp2_mixed(float (&x)[N], int count) {
+    static_assert(POLY % 2 == 0 && POLY <= 8, "pairs");
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        const bool up = (lane & o) != 0;
+    for (int j = 0; j < N; j += 8) {
+        if (j >= count) break;
 #pragma unroll
-        for (int i = 0; i < o; ++i) {
-            const float lo = e[BASE + i], hi = e[BASE + i + o];
-            const float send = up ? lo : hi;
-            const float keep = up ? hi : lo;
-            e[BASE + i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        for (int u = 0; u < 8 - POLY; ++u)
+            if (j + u < N && j + u < count) x[j + u] = ex2(x[j + u]);
+#pragma unroll
+        for (int u = 8 - POLY; u < 8; u += 2) {
+            if (j + u + 1 < N && j + u + 1 < count) exp2_poly2(x[j + u], x[j + u + 1]);
+            else if (j + u < N && j + u < count) x[j + u] = ex2(x[j + u]);
         }
     }
-    return e[BASE];
 }
 
-template <int PAD>
-__device__ __forceinline__ void pool_exp(float (&v)[kTile], float sl, float lw) {
-    // v: raw logits of 128 loaded keys (masked keys = -inf).  Output column c in
-    // [PAD, PAD + STEP) is written to v[c - PAD] as exp2(max(v[c-PAD..c+PAD]) * sl - lw).
-    constexpr int STEP = kTile - 2 * PAD;
-    if constexpr (PAD == 0) {
+// in-place max-pool of width 2*PAD+1: v[o] = max(v[o .. o + 2 PAD]) for o < NOUT
+template <int PAD, int NV, int NOUT>
+__device__ __forceinline__ void pool_inplace(float (&v)[NV]) {
+    static_assert(NOUT + 2 * PAD <= NV, "halo");
+    if constexpr (PAD == 1) {
 #pragma unroll
-        for (int c = 0; c < STEP; ++c) v[c] = ex2(fmaf(v[c], sl, -lw));
-    } else if constexpr (PAD == 1) {
+        for (int o = 0; o < NOUT; ++o) v[o] = max3(v[o], v[o + 1], v[o + 2]);
+    } else if constexpr (PAD >= 2) {
+        // b[j] = max(v[j..j+2]); v[j] is dead once b[j] exists
 #pragma unroll
-        for (int c = 0; c < STEP; ++c) v[c] = ex2(fmaf(max3(v[c], v[c + 1], v[c + 2]), sl, -lw));
-    } else {
-        // b[j] = max(v[j], v[j+1], v[j+2]) in place (v[j] is dead once b[j] exists)
-#pragma unroll
-        for (int j = 0; j < kTile - 2; ++j) v[j] = max3(v[j], v[j + 1], v[j + 2]);
+        for (int jj = 0; jj < NOUT + 2 * PAD - 2; ++jj) v[jj] = max3(v[jj], v[jj + 1], v[jj + 2]);
         if constexpr (PAD == 2) {
-            // window [c-2, c+2] = b[c-2] | b[c]
 #pragma unroll
-            for (int c = 2; c < 2 + STEP; ++c) v[c - 2] = ex2(fmaf(fmaxf(v[c - 2], v[c]), sl, -lw));
+            for (int o = 0; o < NOUT; ++o) v[o] = fmaxf(v[o], v[o + 2]);
         } else {
-            // PAD == 3: window [c-3, c+3] = b[c-3] | b[c] | b[c+1]; b[c-3] is dead after use
+            static_assert(PAD == 3, "pad <= 3");
 #pragma unroll
-            for (int c = 3; c < 3 + STEP; ++c) v[c - 3] = ex2(fmaf(max3(v[c - 3], v[c], v[c + 1]), sl, -lw));
+            for (int o = 0; o < NOUT; ++o) v[o] = max3(v[o], v[o + 3], v[o + 4]);
         }
     }
+}
+
+// pass-2 epilogue of one 32-output column group CG (outputs [32 CG, min(32 CG + 32, STEP)))
+template <int PAD, int CG>
+__device__ __forceinline__ void pass2_group(uint32_t taddr, int lane, int r, int key_col0, int n_o, float sl,
+                                            float lw2, uint8_t* a2tile, uint64_t* acc_empty_bar,
+                                            uint64_t* e_empty_bar, uint32_t e_parity, uint64_t* e_full_bar) {
+    constexpr int STEP = kTile - 2 * PAD;
+    constexpr int O0 = 32 * CG;                               // first output == first loaded column
+    constexpr int NOUT = (STEP - O0) < 32 ? (STEP - O0) : 32; // outputs of this group
+    constexpr int NV = (CG < 3 && PAD > 0) ? 40 : 32;         // loaded columns incl. the halo
+    float v[NV];
+    tmem_ld_x32<0>(taddr + O0, v);
+    if constexpr (NV > 32) tmem_ld_x8<32>(taddr + O0 + 32, v);
+    tmem_ld_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(acc_empty_bar);
+    // keys outside [0, n_o) are excluded from every window (padded cells, policies.hpp:105-106)
+    const int k0 = key_col0 + O0;
+    if (k0 < 0 || k0 + NV > n_o) {
+#pragma unroll
+        for (int jj = 0; jj < NV; ++jj)
+            if (k0 + jj < 0 || k0 + jj >= n_o) v[jj] = -INFINITY;
+    }
+    pool_inplace<PAD, NV, NOUT>(v);
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) v[o] = ex2(fmaf(v[o], sl, -lw2));
+    // E^T tile (fp16, MN-major SW128): window row r = K index, output o = M index
+    mbar_wait(e_empty_bar, e_parity);
+    uint8_t* rowbase = a2tile + (r >> 3) * 2048 + (CG >> 1) * 1024 + (r & 7) * 128;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        uint32_t w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int o0 = c * 8 + 2 * u, o1 = o0 + 1;
+            const float e0 = o0 < NOUT ? v[o0 < NOUT ? o0 : 0] : 0.f;
+            const float e1 = o1 < NOUT ? v[o1 < NOUT ? o1 : 0] : 0.f;
+            const __half2 h2 = __floats2half2_rn(e0, e1);
+            w[u] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+        const int chunk = 4 * (CG & 1) + c;
+        *reinterpret_cast<uint4*>(rowbase + ((chunk ^ (r & 7)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(e_full_bar);
 }
 
 template <int PAD>
@@ -125,6 +184,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     extern __shared__ uint8_t smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool pass2 = prm.pass == 2;
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tm_q);
@@ -133,15 +193,29 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             mbar_init(&S.full[s], 1);
             mbar_init(&S.empty[s], 1);
         }
+        mbar_init(&S.q_full, 1);
+        mbar_init(&S.q_empty, 1);
         for (int b = 0; b < 2; ++b) {
-            mbar_init(&S.q_full[b], 1);
-            mbar_init(&S.q_empty[b], 1);
             mbar_init(&S.acc_full[b], 1);
-            mbar_init(&S.acc_empty[b], 4);
+            mbar_init(&S.acc_empty[b], kEpiWarps);
+            mbar_init(&S.e_full[b], kEpiWarps);  // every column group writes its slice of E^T
+            mbar_init(&S.e_empty[b], 1);
+            mbar_init(&S.d2_full[b], 1);
+            mbar_init(&S.d2_empty[b], 4);
         }
         mbar_fence_init();
     }
     if (warp == 1) tmem_alloc<kTmemCols>(&S.tmem_base);
+    if (pass2) {
+        // head-indicator B operand: Hd[row k][head n] = 1 iff k / m == n < g (K-major, SW128)
+        for (int i = threadIdx.x; i < 2 * 16 * 64; i += kThreads) {
+            const int hk = i / (16 * 64), n = (i / 64) % 16, kk = i % 64;
+            const int krow = hk * 64 + kk;
+            const __half val = __float2half((n < prm.gs && krow / prm.m == n) ? 1.f : 0.f);
+            *reinterpret_cast<__half*>(&S.b2[hk][n * 128 + (((kk >> 3) ^ (n & 7)) << 4) + (kk & 7) * 2]) = val;
+        }
+        fence_async_smem();
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -150,19 +224,24 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     if (warp == 0) {
         // ===================== TMA producer =====================
         if (lane == 0) {
-            const uint64_t pol = prm.pass == 1 ? policy_evict_last() : policy_evict_first();
+            const uint64_t pol = pass2 ? policy_evict_first() : policy_evict_last();
             const uint64_t pol_q = policy_evict_last();
-            uint32_t stage = 0, sphase = 0, qb = 0, qphase = 0;
+            uint32_t stage = 0, sphase = 0, qphase = 0;
+            long long prod_wait = 0;
+            const long long p_start = clock64();
             for (int item = blockIdx.x; item < prm.n_items; item += gridDim.x) {
                 const int pg = item / prm.chunks_per_pg, chunk = item % prm.chunks_per_pg;
                 const int t0 = chunk * prm.tiles_per_item;
                 const int t1 = min(t0 + prm.tiles_per_item, prm.tiles_per_pg);
-                mbar_wait(&S.q_empty[qb], qphase ^ 1);
-                mbar_arrive_expect_tx(&S.q_full[qb], kTileBytes);
-                tma_load_3d(S.q[qb][0], &tm_q, 0, 0, pg, &S.q_full[qb], pol_q);
-                tma_load_3d(S.q[qb][1], &tm_q, 64, 0, pg, &S.q_full[qb], pol_q);
+                mbar_wait(&S.q_empty, qphase ^ 1);
+                qphase ^= 1;
+                mbar_arrive_expect_tx(&S.q_full, kTileBytes);
+                tma_load_3d(S.q[0], &tm_q, 0, 0, pg, &S.q_full, pol_q);
+                tma_load_3d(S.q[1], &tm_q, 64, 0, pg, &S.q_full, pol_q);
                 for (int t = t0; t < t1; ++t) {
+                    const long long w0 = clock64();
                     mbar_wait(&S.empty[stage], sphase ^ 1);
+                    prod_wait += clock64() - w0;
                     mbar_arrive_expect_tx(&S.full[stage], kTileBytes);
                     const int row = t * prm.step - prm.pad;
                     tma_load_3d(S.k[stage][0], &tm_k, 0, row, pg, &S.full[stage], pol);
@@ -172,33 +251,57 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                         sphase ^= 1;
                     }
                 }
-                if (++qb == 2) {
-                    qb = 0;
-                    qphase ^= 1;
-                }
+            }
+            if (prm.debug & 32) {
+                long long* ts = reinterpret_cast<long long*>(prm.head_scores) + blockIdx.x * 8;
+                ts[0] = prod_wait;
+                ts[1] = clock64() - p_start;
             }
         }
     } else if (warp == 1) {
         // ===================== tcgen05 MMA issuer =====================
         if (lane == 0) {
-            constexpr uint32_t idesc = idesc_bf16_f32(128, kTile);
-            uint32_t stage = 0, sphase = 0, qb = 0, qphase = 0, ab = 0, aphase = 0;
+            constexpr uint32_t idesc1 = idesc_bf16_f32(128, kTile);
+            constexpr uint32_t idesc2 = idesc_f16_f32(128, 16, 1);
+            uint32_t stage = 0, sphase = 0, qphase = 0;
+            uint32_t j = 0;  // tile sequence number of this CTA
+            long long mma_wait_acc = 0, mma_wait_full = 0;
+            auto mma2 = [&](uint32_t i) {
+                const uint32_t b = i & 1, ph = (i >> 1) & 1;
+                mbar_wait(&S.e_full[b], ph);
+                mbar_wait(&S.d2_empty[b], ph ^ 1);
+                tc_fence_after();
+#pragma unroll
+                for (int s = 0; s < 8; ++s) {
+                    const uint64_t ad = desc_mnmajor_sw128(smem_u32(S.a2[b]) + s * 4096, 1024, 2048);
+                    const uint64_t bd = desc_kmajor_sw128(smem_u32(S.b2[s >> 2]) + (s & 3) * 32);
+                    mma_f16(tmem + kD2Col + 16 * b, ad, bd, idesc2, s > 0 ? 1u : 0u);
+                }
+                mma_commit(&S.e_empty[b]);
+                mma_commit(&S.d2_full[b]);
+            };
             for (int item = blockIdx.x; item < prm.n_items; item += gridDim.x) {
                 const int chunk = item % prm.chunks_per_pg;
                 const int t0 = chunk * prm.tiles_per_item;
                 const int t1 = min(t0 + prm.tiles_per_item, prm.tiles_per_pg);
-                mbar_wait(&S.q_full[qb], qphase);
-                for (int t = t0; t < t1; ++t) {
-                    mbar_wait(&S.acc_empty[ab], aphase ^ 1);
+                mbar_wait(&S.q_full, qphase);
+                qphase ^= 1;
+                for (int t = t0; t < t1; ++t, ++j) {
+                    const uint32_t ab = j & 1, aph = (j >> 1) & 1;
+                    long long w0 = clock64();
+                    mbar_wait(&S.acc_empty[ab], aph ^ 1);
+                    mma_wait_acc += clock64() - w0;
+                    w0 = clock64();
                     mbar_wait(&S.full[stage], sphase);
+                    mma_wait_full += clock64() - w0;
                     tc_fence_after();
                     const uint32_t d = tmem + ab * kTile;
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk) {
                         const uint32_t off = (kk & 3) * 32;
-                        const uint64_t ad = desc_kmajor_sw128(smem_u32(S.q[qb][kk >> 2]) + off);
+                        const uint64_t ad = desc_kmajor_sw128(smem_u32(S.q[kk >> 2]) + off);
                         const uint64_t bd = desc_kmajor_sw128(smem_u32(S.k[stage][kk >> 2]) + off);
-                        mma_bf16(d, ad, bd, idesc, kk > 0 ? 1u : 0u);
+                        mma_bf16(d, ad, bd, idesc1, kk > 0 ? 1u : 0u);
                     }
                     mma_commit(&S.empty[stage]);
                     mma_commit(&S.acc_full[ab]);
@@ -206,130 +309,206 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                         stage = 0;
                         sphase ^= 1;
                     }
-                    if (++ab == 2) {
-                        ab = 0;
-                        aphase ^= 1;
-                    }
+                    if (pass2 && j > 0) mma2(j - 1);
                 }
-                mma_commit(&S.q_empty[qb]);
-                if (++qb == 2) {
-                    qb = 0;
-                    qphase ^= 1;
-                }
+                mma_commit(&S.q_empty);
+            }
+            if (pass2 && j > 0) mma2(j - 1);
+            if (prm.debug & 32) {
+                long long* ts = reinterpret_cast<long long*>(prm.head_scores) + blockIdx.x * 8;
+                ts[2] = mma_wait_acc;
+                ts[3] = mma_wait_full;
             }
         }
     } else {
-        // ===================== epilogue (warps 2..5) =====================
-        const int quarter = warp & 3;               // TMEM lane quarter this warp may access
-        const int r = quarter * 32 + lane;          // window row == TMEM lane
-        const int R = prm.gs * prm.m;
-        const bool active = r < R;
-        const int et = (warp - 2) * 32 + lane;      // 0..127 epilogue thread id
+        // ===================== epilogue (warps 2..9) =====================
+        const int ew = warp - 2;
+        const int q = warp & 3;              // TMEM lane quarter == head (m == 32)
+        const int cg = ew >> 2;              // 32-column group
+        const int r = q * 32 + lane;         // window row == TMEM lane
+        const bool active = r < prm.gs * prm.m;
+        const int et = ew * 32 + lane;       // 0..511
         const float sl = prm.scale_log2;
-        uint32_t ab = 0, aphase = 0, hb = 0;
+        uint32_t j = 0;
+        long long epi_wait = 0;
+        const long long e_start = clock64();
+        int prev_pg = -1, prev_t = 0;
+        auto readout = [&](uint32_t i, int rpg, int rt) {
+            // D2 of tile i: lanes = output keys, columns = heads (one warp per lane quarter)
+            const uint32_t b = i & 1, ph = (i >> 1) & 1;
+            mbar_wait(&S.d2_full[b], ph);
+            tc_fence_after();
+            float hv[16];
+            tmem_ld_x16<0>(tmem + kD2Col + 16 * b + (uint32_t(q * 32) << 16), hv);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.d2_empty[b]);
+            const int o = q * 32 + lane;
+            const int key = rt * prm.step + o;
+            if (o < prm.step && key < prm.n_o) {
+                const int gpg = prm.pg_base + rpg;
+                const int p = gpg / prm.G, g = gpg % prm.G;
+                constexpr float inv_scale = 1.f / 65536.f;
+                float gsum = 0.f;
+#pragma unroll
+                for (int h = 0; h < 16; ++h) {
+                    if (h >= prm.gs) break;
+                    const float sh = hv[h] * inv_scale;
+                    gsum += sh;
+                    if (prm.head_scores)
+                        prm.head_scores[(size_t(p) * prm.H + g * prm.gs + h) * prm.n_o + key] = sh;
+                }
+                prm.group_scores[size_t(gpg) * prm.n_o + key] = gsum * prm.inv_g;
+            }
+        };
         for (int item = blockIdx.x; item < prm.n_items; item += gridDim.x) {
             const int pg = item / prm.chunks_per_pg, chunk = item % prm.chunks_per_pg;
             const int t0 = chunk * prm.tiles_per_item;
             const int t1 = min(t0 + prm.tiles_per_item, prm.tiles_per_pg);
             const int gpg = prm.pg_base + pg;
-            float run_m = -INFINITY, run_s = 0.f, lw = INFINITY;
-            if (prm.pass == 2 && active) lw = prm.final_stats[(size_t(gpg) * 128 + r) * 2 + 1];
-            for (int t = t0; t < t1; ++t) {
-                mbar_wait(&S.acc_full[ab], aphase);
+            float run_m = -INFINITY, run_s = 0.f, lw2 = INFINITY;
+            if (pass2 && active) lw2 = prm.final_stats[(size_t(gpg) * 128 + r) * 2 + 1] - kEScaleLog2;
+            for (int t = t0; t < t1; ++t, ++j) {
+                const uint32_t ab = j & 1, aph = (j >> 1) & 1;
+                const long long w0 = clock64();
+                mbar_wait(&S.acc_full[ab], aph);
+                epi_wait += clock64() - w0;
                 tc_fence_after();
-                float v[kTile];
-                const uint32_t taddr = tmem + ab * kTile + (uint32_t(quarter * 32) << 16);
-                tmem_ld_x32<0>(taddr + 0, v);
-                tmem_ld_x32<32>(taddr + 32, v);
-                tmem_ld_x32<64>(taddr + 64, v);
-                tmem_ld_x32<96>(taddr + 96, v);
-                tmem_ld_wait();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&S.acc_empty[ab]);
-                if (++ab == 2) {
-                    ab = 0;
-                    aphase ^= 1;
-                }
-                const int key0 = t * prm.step - prm.pad;
-                if (prm.pass == 1) {
-                    const int nvalid = min(kTile, prm.n_o - key0);
-                    if (nvalid < kTile) {
+                const uint32_t taddr = tmem + ab * kTile + (uint32_t(q * 32) << 16);
+                if (!pass2) {
+                    float v[32];
+                    tmem_ld_x32<0>(taddr + 32 * cg, v);
+                    tmem_ld_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&S.acc_empty[ab]);
+                    const int nvalid = prm.n_o - (t * kTile + 32 * cg);
+                    if (nvalid < 32) {
 #pragma unroll
-                        for (int j = 0; j < kTile; ++j)
-                            if (j >= nvalid) v[j] = -INFINITY;
+                        for (int c = 0; c < 32; ++c)
+                            if (c >= nvalid) v[c] = -INFINITY;
                     }
-                    float tm = v[0];
+                    float m2[2];
 #pragma unroll
-                    for (int j = 1; j + 1 < kTile; j += 2) tm = max3(tm, v[j], v[j + 1]);
-                    tm = fmaxf(tm, v[kTile - 1]);
-                    const float nm = fmaxf(run_m, tm * sl);
-                    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+                    for (int c = 0; c < 2; ++c) {
+                        float mm = max3(v[16 * c], v[16 * c + 1], v[16 * c + 2]);
 #pragma unroll
-                    for (int j = 0; j < kTile; j += 4) {
-                        s0 += ex2(fmaf(v[j + 0], sl, -nm));
-                        s1 += ex2(fmaf(v[j + 1], sl, -nm));
-                        s2 += ex2(fmaf(v[j + 2], sl, -nm));
-                        s3 += ex2(fmaf(v[j + 3], sl, -nm));
+                        for (int u = 3; u < 15; u += 2) mm = max3(mm, v[16 * c + u], v[16 * c + u + 1]);
+                        m2[c] = fmaxf(mm, v[16 * c + 15]);
                     }
-                    run_s = run_s * ex2(run_m - nm) + ((s0 + s1) + (s2 + s3));
-                    run_m = nm;
-                } else {
-                    if (key0 < 0 || key0 + kTile > prm.n_o) {
+                    const float tmx = fmaxf(m2[0], m2[1]);
+                    const float nm = fmaxf(run_m, tmx * sl);
+                    if (nm != -INFINITY) {
 #pragma unroll
-                        for (int j = 0; j < kTile; ++j)
-                            if (key0 + j < 0 || key0 + j >= prm.n_o) v[j] = -INFINITY;
-                    }
-                    pool_exp<PAD>(v, sl, active ? lw : INFINITY);
-                    constexpr int STEP = kTile - 2 * PAD;
+                        for (int c = 0; c < 32; ++c) v[c] = fmaf(v[c], sl, -nm);
+                        if (prm.debug & 64) exp2_mixed<32, 2>(v, 32);
+                        else if (prm.debug & 128) exp2_mixed<32, 4>(v, 32);
+                        else exp2_mixed<32, 0>(v, 32);
+                        uint64_t a0 = pk(0.f, 0.f), a1 = pk(0.f, 0.f);
 #pragma unroll
-                    for (int c = STEP; c < kTile; ++c) v[c] = 0.f;
-                    float* hp = S.head_part[hb][quarter];
-                    hp[0 + lane] = butterfly32<0>(v, lane);
-                    hp[32 + lane] = butterfly32<32>(v, lane);
-                    hp[64 + lane] = butterfly32<64>(v, lane);
-                    hp[96 + lane] = butterfly32<96>(v, lane);
-                    named_bar(1, 128);
-                    // heads -> group mean; one key per epilogue thread, coalesced stores
-                    const int key = t * prm.step + et;
-                    if (et < STEP && key < prm.n_o) {
-                        const int p = gpg / prm.G, g = gpg % prm.G;
-                        float gsum = 0.f;
-                        for (int h = 0; h < prm.gs; ++h) {
-                            const float hv = S.head_part[hb][h][et];
-                            gsum += hv;
-                            if (prm.head_scores)
-                                prm.head_scores[(size_t(p) * prm.H + g * prm.gs + h) * prm.n_o + key] = hv;
+                        for (int c = 0; c < 32; c += 4) {
+                            a0 = add2(a0, pk(v[c], v[c + 1]));
+                            a1 = add2(a1, pk(v[c + 2], v[c + 3]));
                         }
-                        prm.group_scores[size_t(gpg) * prm.n_o + key] = gsum * prm.inv_g;
+                        float s0, s1, s2, s3;
+                        upk(a0, s0, s1);
+                        upk(a1, s2, s3);
+                        run_s = (run_m == -INFINITY ? 0.f : run_s * ex2(run_m - nm)) + ((s0 + s1) + (s2 + s3));
+                        run_m = nm;
                     }
-                    hb ^= 1;
+                } else {
+                    const uint32_t eb = j & 1, eph = (j >> 1) & 1;
+                    const int key_col0 = t * prm.step - prm.pad;
+                    const float lw = active ? lw2 : INFINITY;
+                    switch (cg) {
+                        case 0: pass2_group<PAD, 0>(taddr, lane, r, key_col0, prm.n_o, sl, lw, S.a2[eb], &S.acc_empty[ab],
+                                                    &S.e_empty[eb], eph ^ 1, &S.e_full[eb]); break;
+                        case 1: pass2_group<PAD, 1>(taddr, lane, r, key_col0, prm.n_o, sl, lw, S.a2[eb], &S.acc_empty[ab],
+                                                    &S.e_empty[eb], eph ^ 1, &S.e_full[eb]); break;
+                        case 2: pass2_group<PAD, 2>(taddr, lane, r, key_col0, prm.n_o, sl, lw, S.a2[eb], &S.acc_empty[ab],
+                                                    &S.e_empty[eb], eph ^ 1, &S.e_full[eb]); break;
+                        default: pass2_group<PAD, 3>(taddr, lane, r, key_col0, prm.n_o, sl, lw, S.a2[eb], &S.acc_empty[ab],
+                                                     &S.e_empty[eb], eph ^ 1, &S.e_full[eb]); break;
+                    }
+                    // the last column group (fewest outputs) reads back the previous tile's scores
+                    if (cg == 3 && j > 0) readout(j - 1, prev_pg, prev_t);
+                    prev_pg = pg;
+                    prev_t = t;
                 }
             }
-            if (prm.pass == 1) {
-                float* pp = prm.partial + ((size_t(pg) * prm.chunks_per_pg + chunk) * 128 + r) * 2;
+            if (!pass2) {
+                float* pp = prm.partial + (((size_t(pg) * prm.chunks_per_pg + chunk) * 4 + cg) * 128 + r) * 2;
                 pp[0] = active ? run_m : -INFINITY;
                 pp[1] = active ? run_s : 0.f;
-                __threadfence();
-                named_bar(1, 128);
-                if (et == 0) S.is_last = atomicAdd(&prm.tickets[pg], 1u) == unsigned(prm.chunks_per_pg - 1);
-                named_bar(1, 128);
-                if (S.is_last) {
-                    __threadfence();
-                    const float* base = prm.partial + size_t(pg) * prm.chunks_per_pg * 256;
-                    float M = -INFINITY;
-                    for (int c = 0; c < prm.chunks_per_pg; ++c) M = fmaxf(M, __ldcg(base + (c * 128 + r) * 2));
-                    float Ssum = 0.f;
-                    for (int c = 0; c < prm.chunks_per_pg; ++c) {
-                        const float mc = __ldcg(base + (c * 128 + r) * 2);
-                        if (mc != -INFINITY) Ssum += __ldcg(base + (c * 128 + r) * 2 + 1) * ex2(mc - M);
+                if (prm.debug & 4) continue;
+                // grid-sync pattern: CTA barrier, then ONE thread fences (cumulative release of
+                // every epilogue thread's partial) and takes the ticket (a fence per thread costs
+                // ~0.5 ms here); the last arriver fences again (acquire) before the fold.
+                named_bar(1, 32 * kEpiWarps);
+                if (et == 0) {
+                    if (!(prm.debug & 8)) __threadfence();
+                    const bool last = atomicAdd(&prm.tickets[pg], 1u) == unsigned(prm.chunks_per_pg - 1);
+                    if (last && !(prm.debug & 8)) __threadfence();
+                    S.is_last = last;
+                }
+                named_bar(1, 32 * kEpiWarps);
+                if (S.is_last && !(prm.debug & 16)) {
+                    // parallel fold: thread (row r, column group cg) folds every 4th partial of
+                    // its row (all loads in flight at once), then the 4 groups merge via smem.
+                    const float* base = prm.partial + size_t(pg) * prm.chunks_per_pg * 4 * 256;
+                    const int nparts = prm.chunks_per_pg * 4;
+                    float M = -INFINITY, Ssum = 0.f;
+                    for (int c0 = cg; c0 < nparts; c0 += 32) {
+                        float2 v8[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int c = c0 + 4 * u;
+                            v8[u] = c < nparts ? __ldcg(reinterpret_cast<const float2*>(base + (c * 128 + r) * 2))
+                                               : make_float2(-INFINITY, 0.f);
+                        }
+                        float bm = M;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) bm = fmaxf(bm, v8[u].x);
+                        if (bm != -INFINITY) {
+                            float acc = M == -INFINITY ? 0.f : Ssum * ex2(M - bm);
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                if (v8[u].x != -INFINITY) acc += v8[u].y * ex2(v8[u].x - bm);
+                            Ssum = acc;
+                            M = bm;
+                        }
                     }
-                    float* fs = prm.final_stats + (size_t(gpg) * 128 + r) * 2;
-                    fs[0] = M;
-                    fs[1] = active ? M + __log2f(Ssum) + prm.log2_m : INFINITY;
-                    if (et == 0) prm.tickets[pg] = 0u;
+                    // stash in the (now idle) E^T staging buffer: [cg][128 rows][2]
+                    float* red = reinterpret_cast<float*>(S.a2[0]);
+                    red[(cg * 128 + r) * 2 + 0] = M;
+                    red[(cg * 128 + r) * 2 + 1] = Ssum;
+                    named_bar(1, 32 * kEpiWarps);
+                    if (cg == 0) {
+                        float Mf = -INFINITY;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) Mf = fmaxf(Mf, red[(c * 128 + r) * 2]);
+                        float Sf = 0.f;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const float mc = red[(c * 128 + r) * 2];
+                            if (mc != -INFINITY) Sf += red[(c * 128 + r) * 2 + 1] * ex2(mc - Mf);
+                        }
+                        float* fs = prm.final_stats + (size_t(gpg) * 128 + r) * 2;
+                        fs[0] = Mf;
+                        fs[1] = active ? Mf + __log2f(Sf) + prm.log2_m : INFINITY;
+                        if (et == 0) prm.tickets[pg] = 0u;
+                    }
+                    named_bar(1, 32 * kEpiWarps);
                 }
             }
+        }
+        if (pass2 && cg == 3 && j > 0) readout(j - 1, prev_pg, prev_t);
+        if ((prm.debug & 32) && et == 0) {
+            long long* ts = reinterpret_cast<long long*>(prm.head_scores) + blockIdx.x * 8;
+            ts[4] = epi_wait;
+            ts[5] = clock64() - e_start;
+            ts[6] = j;
         }
     }
     tc_fence_before();
@@ -348,9 +527,9 @@ EncodeFn get_encode() {
     static std::once_flag once;
     std::call_once(once, [] {
         void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+            qr == cudaDriverEntryPointSuccess)
             fn = reinterpret_cast<EncodeFn>(p);
     });
     return fn;
@@ -373,10 +552,27 @@ adakv_status make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t 
 
 size_t smem_bytes() { return sizeof(Smem) + 1024; }
 
+// Tiles per item minimising the makespan: ceil(items / CTAs) items per CTA, each costing its
+// tiles plus ~2 tiles of fixed overhead (Q load, pipeline ramp, ticket), plus the serial fold
+// of chunks partials per group in the last CTA (~1 tile per 16 chunks).
+void balance(int64_t pgs, int64_t tiles, int sms, int* tpi, int* chunks) {
+    int64_t best_t = 1, best_cost = INT64_MAX;
+    for (int64_t t = 1; t <= tiles; ++t) {
+        const int64_t ch = ceil_div(tiles, t);
+        const int64_t items = pgs * ch;
+        const int64_t cost = 16 * ceil_div(items, sms) * (t + 2) + ch;
+        if (cost < best_cost) {
+            best_cost = cost;
+            best_t = t;
+        }
+    }
+    *tpi = int(best_t);
+    *chunks = int(ceil_div(tiles, best_t));
+}
+
 struct Plan {
-    int64_t slice;       // problems per slice (L2-resident pass pair)
-    int chunks1, tpi1;   // pass 1 decomposition per (p, g)
-    int chunks2, tpi2;
+    int64_t slice;
+    int tpi1, chunks1, tpi2, chunks2;
 };
 
 Plan make_plan(const adakv_layer_shape& s, int pad) {
@@ -384,14 +580,9 @@ Plan make_plan(const adakv_layer_shape& s, int pad) {
     const int64_t k_bytes = s.kv_groups * (s.outside + s.window) * s.head_dim * 2;
     pl.slice = std::max<int64_t>(1, std::min<int64_t>(s.problems, (48ll << 20) / std::max<int64_t>(k_bytes, 1)));
     const int sms = device_sm_count();
-    const int step2 = kTile - 2 * pad;
-    const int64_t tiles1 = ceil_div(s.outside, kTile), tiles2 = ceil_div(s.outside, step2);
     const int64_t pgs = pl.slice * s.kv_groups;
-    // aim for ~4 items per CTA so the persistent grid balances
-    pl.tpi1 = int(std::max<int64_t>(1, (pgs * tiles1) / (int64_t(sms) * 4)));
-    pl.tpi2 = int(std::max<int64_t>(1, (pgs * tiles2) / (int64_t(sms) * 4)));
-    pl.chunks1 = int(ceil_div(tiles1, pl.tpi1));
-    pl.chunks2 = int(ceil_div(tiles2, pl.tpi2));
+    balance(pgs, ceil_div(s.outside, kTile), sms, &pl.tpi1, &pl.chunks1);
+    balance(pgs, ceil_div(s.outside, kTile - 2 * pad), sms, &pl.tpi2, &pl.chunks2);
     return pl;
 }
 
@@ -405,11 +596,10 @@ bool score_window_tc_supported(adakv_dtype dt, const adakv_layer_shape& s, int64
 }
 
 size_t score_window_tc_workspace(const adakv_layer_shape& s) {
-    const Plan pl = make_plan(s, 3);
+    const Plan pl = make_plan(s, 0);
     const int64_t pgs_slice = pl.slice * s.kv_groups;
-    const int64_t chunks = std::max(pl.chunks1, make_plan(s, 0).chunks1);
-    return 3 * 256 + size_t(pgs_slice) * chunks * 128 * 2 * 4 + size_t(s.problems * s.kv_groups) * 128 * 2 * 4 +
-           size_t(pgs_slice) * 4;
+    return 3 * 256 + size_t(pgs_slice) * pl.chunks1 * 4 * 128 * 2 * 4 +
+           size_t(s.problems * s.kv_groups) * 128 * 2 * 4 + size_t(pgs_slice) * 4;
 }
 
 adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, int32_t scale, const void* q,
@@ -419,17 +609,15 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
     const int64_t G = s.kv_groups, H = s.q_heads, gs = H / G, m = s.window, n = s.outside + s.window;
     const int64_t d = s.head_dim;
     Arena ar(ws);
-    const Plan pl0 = make_plan(s, 0);
-    const int64_t chunks_max = std::max(pl.chunks1, pl0.chunks1);
-    float* partial = ar.take<float>(size_t(pl.slice * G * chunks_max * 256));
+    float* partial = ar.take<float>(size_t(pl.slice * G * pl.chunks1 * 4 * 256));
     float* fstats = ar.take<float>(size_t(s.problems * G * 256));
     unsigned* tickets = ar.take<unsigned>(size_t(pl.slice * G));
     ADAKV_CUDA_TRY(cudaMemsetAsync(tickets, 0, size_t(pl.slice * G) * 4, stream));
     const size_t smem = smem_bytes();
     const int sms = device_sm_count();
-    auto kfn = pad == 0 ? score_tc_kernel<0> : pad == 1 ? score_tc_kernel<1> : pad == 2 ? score_tc_kernel<2>
-                                                                                        : score_tc_kernel<3>;
-    ADAKV_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    auto k2 = pad == 0 ? score_tc_kernel<0> : pad == 1 ? score_tc_kernel<1> : pad == 2 ? score_tc_kernel<2>
+                                                                                       : score_tc_kernel<3>;
+    ADAKV_CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ADAKV_CUDA_TRY(cudaFuncSetAttribute(score_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const float sc = scale ? 1.0f / sqrtf(float(d)) : 1.0f;
     for (int64_t p0 = 0; p0 < s.problems; p0 += pl.slice) {
@@ -454,13 +642,18 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
         prm.tickets = tickets;
         prm.head_scores = static_cast<float*>(head_scores);
         prm.group_scores = static_cast<float*>(group_scores);
+        static const int dbg = [] {
+            const char* e = std::getenv("ADAKV_TC_DEBUG");
+            return e ? std::atoi(e) : 0;
+        }();
+        prm.debug = dbg;
         // pass 1: row statistics over 128-key tiles
         prm.pass = 1;
         prm.step = kTile;
         prm.pad = 0;
         prm.tiles_per_pg = int(ceil_div(s.outside, kTile));
-        prm.tiles_per_item = pl0.tpi1;
-        prm.chunks_per_pg = pl0.chunks1;
+        prm.tiles_per_item = pl.tpi1;
+        prm.chunks_per_pg = pl.chunks1;
         prm.n_items = int(np * G * prm.chunks_per_pg);
         int grid = std::min(prm.n_items, sms);
         score_tc_kernel<0><<<grid, kThreads, smem, stream>>>(tq, tk, prm);
@@ -474,7 +667,8 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
         prm.chunks_per_pg = pl.chunks2;
         prm.n_items = int(np * G * prm.chunks_per_pg);
         grid = std::min(prm.n_items, sms);
-        kfn<<<grid, kThreads, smem, stream>>>(tq, tk, prm);
+        if (dbg & 1) continue;  // debug: pass 1 only
+        k2<<<grid, kThreads, smem, stream>>>(tq, tk, prm);
         ADAKV_CUDA_TRY(cudaGetLastError());
     }
     return ADAKV_OK;

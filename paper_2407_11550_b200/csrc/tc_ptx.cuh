@@ -145,5 +145,108 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+template <int OFF, int N>
+__device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, float (&v)[N]) {
+    static_assert(OFF + 16 <= N, "range");
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+        : "=f"(v[OFF + 0]), "=f"(v[OFF + 1]), "=f"(v[OFF + 2]), "=f"(v[OFF + 3]), "=f"(v[OFF + 4]),
+          "=f"(v[OFF + 5]), "=f"(v[OFF + 6]), "=f"(v[OFF + 7]), "=f"(v[OFF + 8]), "=f"(v[OFF + 9]),
+          "=f"(v[OFF + 10]), "=f"(v[OFF + 11]), "=f"(v[OFF + 12]), "=f"(v[OFF + 13]), "=f"(v[OFF + 14]),
+          "=f"(v[OFF + 15])
+        : "r"(taddr));
+}
+template <int OFF, int N>
+__device__ __forceinline__ void tmem_ld_x8(uint32_t taddr, float (&v)[N]) {
+    static_assert(OFF + 8 <= N, "range");
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(v[OFF + 0]), "=f"(v[OFF + 1]), "=f"(v[OFF + 2]), "=f"(v[OFF + 3]), "=f"(v[OFF + 4]),
+                   "=f"(v[OFF + 5]), "=f"(v[OFF + 6]), "=f"(v[OFF + 7])
+                 : "r"(taddr));
+}
+
+// MN-major operand, 128-byte swizzle: atoms of 64 MN-elements (128 B) x 8 K-rows;
+// lbo = byte stride between MN-atoms, sbo = byte stride between K-atoms.
+__device__ __forceinline__ uint64_t desc_mnmajor_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFFu);
+    d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
+    d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(2) << 61;
+    return d;
+}
+
+// kind::f16 with F16 A/B, F32 D; A major selectable (1 = MN-major), B K-major.
+__host__ __device__ constexpr uint32_t idesc_f16_f32(uint32_t M, uint32_t N, uint32_t a_mn_major) {
+    return (1u << 4) | (0u << 7) | (0u << 10) | (a_mn_major << 15) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// make generic-proxy shared-memory writes visible to the async proxy (tensor core / TMA)
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- packed fp32x2
+__device__ __forceinline__ uint64_t pk(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void upk(uint64_t v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// 2^x for two lanes on the FMA pipe (FA4-style MUFU offload): x = n + f, n = rint(x) by the
+// 1.5*2^23 trick, f in [-0.5, 0.5], degree-6 Taylor of 2^f (|rel err| < 2e-7), exponent
+// added as integer bits.  Inputs are clamped to >= -125 so the result stays normal (2^-125 ~ 2e-38
+// where MUFU would flush to 0 -- harmless for sums and exactly 0 once rounded to fp16).
+__device__ __forceinline__ void exp2_poly2(float& a, float& b) {
+    a = fmaxf(a, -125.f);
+    b = fmaxf(b, -125.f);
+    const uint64_t magic = pk(12582912.f, 12582912.f);
+    const uint64_t x = pk(a, b);
+    const uint64_t t = add2(x, magic);                        // rint(x) + 1.5*2^23
+    const uint64_t r = add2(t, pk(-12582912.f, -12582912.f)); // rint(x)
+    float r0, r1;
+    upk(r, r0, r1);
+    const uint64_t f = add2(x, pk(-r0, -r1));                 // f = x - rint(x)
+    uint64_t p = pk(1.5403530e-4f, 1.5403530e-4f);
+    p = fma2(p, f, pk(1.3333558e-3f, 1.3333558e-3f));
+    p = fma2(p, f, pk(9.6181291e-3f, 9.6181291e-3f));
+    p = fma2(p, f, pk(5.5504109e-2f, 5.5504109e-2f));
+    p = fma2(p, f, pk(2.4022651e-1f, 2.4022651e-1f));
+    p = fma2(p, f, pk(6.9314718e-1f, 6.9314718e-1f));
+    p = fma2(p, f, pk(1.f, 1.f));
+    float p0, p1, t0, t1;
+    upk(p, p0, p1);
+    upk(t, t0, t1);
+    a = __int_as_float(__float_as_int(p0) + ((__float_as_int(t0) - 0x4B400000) << 23));
+    b = __int_as_float(__float_as_int(p1) + ((__float_as_int(t1) - 0x4B400000) << 23));
+}
+
 }  // namespace ptx
 }  // namespace adakv_b200
