@@ -247,6 +247,37 @@ adakv_status adakv_repair_zero_budgets(int64_t* counts, const int64_t* caps, int
 adakv_status adakv_pyramid_layer_budgets(int64_t per_layer_avg, int64_t num_layers,
                                          double beta_max, double beta_min, int64_t* out);
 
+/* ----------------------------------------------------------------------------
+ * fp64 device kernels behind the reference-typed C++ API (include/adakv_b200/adakv.hpp).
+ * All pointers DEVICE, stream-ordered; loop orders follow the reference without FMA.
+ * ------------------------------------------------------------------------- */
+/* matmul (matrix.hpp:91-102) for every head: q[h] = x * w[h]; x [m, D], w [H, D, d], q [H, m, d] */
+adakv_status adakv_project_queries_f64(const double* x, const double* w, int64_t H, int64_t m, int64_t D,
+                                       int64_t d, double* q, adakv_stream_t stream);
+/* group_mean_scores (policies.hpp:136-156): scores [h, n] -> out [h/g, n] */
+adakv_status adakv_group_mean_scores_f64(const double* scores, int64_t h, int64_t n, int64_t g, double* out,
+                                         adakv_stream_t stream);
+/* attention_weights (attention.hpp:169-179): q [m, d], k [n, d] -> out [m, n] */
+adakv_status adakv_attention_weights_f64(const double* q, int64_t m, const double* k, int64_t n, int64_t d,
+                                         int32_t scale, double* out, adakv_stream_t stream);
+/* attention_output (attention.hpp:182-196): ragged weight rows w (woff[H+1]), values v (voff[H+1]
+ * rows of dh), wo [H, dh, D] -> y [D]; ctx_ws holds H*dh doubles */
+adakv_status adakv_attention_output_f64(const double* w, const int64_t* woff, const double* v,
+                                        const int64_t* voff, int64_t H, int64_t dh, const double* wo, int64_t D,
+                                        double* ctx_ws, double* y, adakv_stream_t stream);
+/* select_and_compact (flat_cache.hpp:92-120): rows with mask != 0 of each segment, in order.
+ * off / out_off: DEVICE int64 [segments + 1] */
+adakv_status adakv_compact_rows_f64(int64_t segments, const uint8_t* mask, const int64_t* off, const double* src_k,
+                                    const double* src_v, int64_t d, const int64_t* out_off, double* dst_k,
+                                    double* dst_v, adakv_stream_t stream);
+
+/* Device memory helpers so C/C++ callers need nothing but this header (synchronous). */
+adakv_status adakv_device_malloc(void** ptr, size_t bytes);
+adakv_status adakv_device_free(void* ptr);
+adakv_status adakv_memcpy_to_device(void* dst, const void* src, size_t bytes);
+adakv_status adakv_memcpy_to_host(void* dst, const void* src, size_t bytes);
+adakv_status adakv_device_synchronize(void);
+
 #ifdef __cplusplus
 }
 #endif

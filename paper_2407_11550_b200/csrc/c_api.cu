@@ -515,4 +515,25 @@ adakv_status adakv_pyramid_layer_budgets(int64_t per_layer_avg, int64_t num_laye
     return e ? fail(ADAKV_INVALID_ARGUMENT, "apportion: failed") : ADAKV_OK;
 }
 
+adakv_status adakv_device_malloc(void** ptr, size_t bytes) {
+    ADAKV_CUDA_TRY(cudaMalloc(ptr, bytes > 0 ? bytes : 1));
+    return ADAKV_OK;
+}
+adakv_status adakv_device_free(void* ptr) {
+    ADAKV_CUDA_TRY(cudaFree(ptr));
+    return ADAKV_OK;
+}
+adakv_status adakv_memcpy_to_device(void* dst, const void* src, size_t bytes) {
+    if (bytes) ADAKV_CUDA_TRY(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    return ADAKV_OK;
+}
+adakv_status adakv_memcpy_to_host(void* dst, const void* src, size_t bytes) {
+    if (bytes) ADAKV_CUDA_TRY(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    return ADAKV_OK;
+}
+adakv_status adakv_device_synchronize(void) {
+    ADAKV_CUDA_TRY(cudaDeviceSynchronize());
+    return ADAKV_OK;
+}
+
 }  // extern "C"
