@@ -258,7 +258,7 @@ def run_ours(args, cfg):
     import ctypes as C
     st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     A._lib.check(lib.adakv_decode(2, B, H, G, d, 1, C.c_void_p(dq[0, 0].data_ptr()), C.c_void_p(cache.k.data_ptr()),
-                                  C.c_void_p(cache.v.data_ptr()), C.c_void_p(cache.seg_start.data_ptr()),
+                                  C.c_void_p(cache.v.data_ptr()), cache.k.shape[0], C.c_void_p(cache.seg_start.data_ptr()),
                                   C.c_void_p(cache.seqlens.data_ptr()), max_rows, None, None,
                                   C.c_void_p(dg.out[0].data_ptr()), C.c_void_p(dg.ws.data_ptr()), dg.ws.numel(), st))
     torch.cuda.synchronize()
@@ -270,7 +270,7 @@ def run_ours(args, cfg):
                 seg = l * B * G
                 A._lib.check(lib.adakv_decode(
                     2, B, H, G, d, 1, C.c_void_p(dq[s, l].data_ptr()), C.c_void_p(cache.k.data_ptr()),
-                    C.c_void_p(cache.v.data_ptr()), C.c_void_p(cache.seg_start.data_ptr() + 4 * seg),
+                    C.c_void_p(cache.v.data_ptr()), cache.k.shape[0], C.c_void_p(cache.seg_start.data_ptr() + 4 * seg),
                     C.c_void_p(cache.seqlens.data_ptr() + 4 * seg), max_rows, C.c_void_p(dk[s, l].data_ptr()),
                     C.c_void_p(dv[s, l].data_ptr()), C.c_void_p(dg.out[l].data_ptr()), C.c_void_p(dg.ws.data_ptr()),
                     dg.ws.numel(), stream))

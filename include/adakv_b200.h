@@ -205,14 +205,24 @@ adakv_status adakv_gather(adakv_dtype dtype, const adakv_layer_shape* shape, int
  *   part of attention_output, 182-196) for one new token per problem, applied to the
  *   retained cache as in report.hpp:133-144; and append_kv (attention.hpp:126-134).
  *   q          DEVICE [P, H, d]
+ *   k_cache, v_cache  the planes (cache_rows rows of d elements each; the segments'
+ *              seg_start offsets index into them)
  *   k_new,v_new  DEVICE [P, G, d] or NULL: appended at row seqlens (the new token's
  *              own K/V, attended in the same step); seqlens is then incremented on the
  *              device.  Requires seqlens < capacity (caller-reserved).
  *   out        DEVICE [P, H, d] (same dtype as q)
+ * Ordering: back-to-back decodes of DIFFERENT segments on one stream (the layers of a
+ * model-wide plane) overlap through programmatic dependent launch -- the next call's
+ * cache rows stream in while the previous call finishes.  The library tracks its own
+ * launches per stream and never overlaps a decode with its own compress / gather /
+ * append_kv or with a decode of the same segments.  A caller kernel enqueued directly
+ * before adakv_decode must not write that call's cache rows, seg_start or seqlens, or
+ * the caller disables the overlap with adakv_set_decode_overlap(0)
+ * (env ADAKV_DECODE_OVERLAP=0).
  * ------------------------------------------------------------------------- */
 adakv_status adakv_decode(adakv_dtype dtype, int64_t problems, int64_t q_heads,
                           int64_t kv_groups, int64_t head_dim, int32_t scale, const void* q,
-                          void* k_cache, void* v_cache, const int32_t* seg_start,
+                          void* k_cache, void* v_cache, int64_t cache_rows, const int32_t* seg_start,
                           int32_t* seqlens, int64_t max_rows, const void* k_new,
                           const void* v_new, void* out, void* workspace, size_t workspace_bytes,
                           adakv_stream_t stream);
@@ -220,6 +230,10 @@ adakv_status adakv_decode(adakv_dtype dtype, int64_t problems, int64_t q_heads,
  * launch covers ceil(max_rows / chunk) splits so the call can live in a CUDA graph). */
 adakv_status adakv_decode_workspace(int64_t problems, int64_t q_heads, int64_t kv_groups,
                                     int64_t head_dim, int64_t max_rows, size_t* bytes);
+
+/* Enables (1, default) or disables (0) the decode overlap described above; returns the
+ * previous setting. */
+int adakv_set_decode_overlap(int enabled);
 
 /* append_kv (attention.hpp:126-134) alone: one row per segment listed. */
 adakv_status adakv_append_kv(adakv_dtype dtype, int64_t segments, int64_t head_dim,

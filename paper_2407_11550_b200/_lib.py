@@ -70,6 +70,8 @@ def _sig(L):
     L.adakv_set_tensor_core_scoring.argtypes = [C.c_int]
     L.adakv_set_tensor_core_scoring.restype = C.c_int
     L.adakv_workspace_status.argtypes = [VP, VP]
+    L.adakv_set_decode_overlap.argtypes = [C.c_int]
+    L.adakv_set_decode_overlap.restype = C.c_int
     L.adakv_compress.argtypes = [S, C.POINTER(LayerShape), C.POINTER(PolicyConfig), I64, VP, VP, VP, VP, I64,
                                  VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP]
     L.adakv_compress_workspace.argtypes = [S, C.POINTER(LayerShape), C.POINTER(PolicyConfig), PSZ]
@@ -81,7 +83,7 @@ def _sig(L):
                                          VP, I64, VP, SZ, VP]
     L.adakv_segmented_select_workspace.argtypes = [I64, I64, PSZ]
     L.adakv_gather.argtypes = [S, C.POINTER(LayerShape), I64, VP, VP, VP, VP, VP, I64, I64, VP, VP, VP, VP, VP]
-    L.adakv_decode.argtypes = [S, I64, I64, I64, I64, I32, VP, VP, VP, VP, VP, I64, VP, VP, VP, VP, SZ, VP]
+    L.adakv_decode.argtypes = [S, I64, I64, I64, I64, I32, VP, VP, VP, I64, VP, VP, I64, VP, VP, VP, VP, SZ, VP]
     L.adakv_decode_workspace.argtypes = [I64, I64, I64, I64, I64, PSZ]
     L.adakv_append_kv.argtypes = [S, I64, I64, VP, VP, VP, VP, VP, VP, VP]
     L.adakv_apportion.argtypes = [VP, I64, I64, VP, VP]

@@ -34,9 +34,9 @@ adakv_status launch_gather(adakv_dtype dt, const adakv_layer_shape& s, int64_t m
                            void* k_cache, void* v_cache, cudaStream_t stream);
 size_t decode_workspace_bytes(int64_t P, int64_t H, int64_t G, int64_t d, int64_t max_rows, size_t acc);
 adakv_status launch_decode(adakv_dtype dt, int64_t P, int64_t H, int64_t G, int64_t d, int32_t scale,
-                           const void* q, void* kc, void* vc, const int32_t* ss, int32_t* sl,
+                           const void* q, void* kc, void* vc, int64_t cache_rows, const int32_t* ss, int32_t* sl,
                            int64_t max_rows, const void* kn, const void* vn, void* out, void* ws,
-                           cudaStream_t stream);
+                           bool overlap_prev, cudaStream_t stream);
 adakv_status launch_append(adakv_dtype dt, int64_t segments, int64_t d, void* kc, void* vc,
                            const int32_t* ss, int32_t* sl, const void* kn, const void* vn,
                            cudaStream_t stream);
@@ -44,6 +44,45 @@ __global__ void budget_kernel(int op, const double* quotas_in, const int64_t* a_
                               int64_t total, double alpha, double bmax, double bmin,
                               const int64_t* caps_in, int64_t* out, double* quotas,
                               uint64_t* caps, uint64_t* tmp_a, uint64_t* tmp_o, uint32_t* err);
+
+// ---------------------------------------------------------------- launch ordering
+// The decode kernel reads its segments' rows and lengths before griddepcontrol.wait, so it
+// may overlap (programmatic dependent launch) only a predecessor that does not write them:
+// a decode of OTHER segments (the next layer of a model-wide plane).  Every entry point
+// that writes cache planes records itself here per stream; decode overlaps only when the
+// previous recorded launch on its stream was a decode on different segments.
+namespace {
+std::mutex g_order_mu;
+struct LastLaunch {
+    cudaStream_t stream;
+    const void* decode_segments;  // nullptr: not a decode
+};
+std::vector<LastLaunch> g_last_launch;
+std::atomic<int> g_decode_overlap{-1};
+}  // namespace
+
+static const void* exchange_last_launch(cudaStream_t s, const void* decode_segments) {
+    std::lock_guard<std::mutex> lock(g_order_mu);
+    for (auto& e : g_last_launch)
+        if (e.stream == s) {
+            const void* prev = e.decode_segments;
+            e.decode_segments = decode_segments;
+            return prev;
+        }
+    if (g_last_launch.size() > 64) g_last_launch.erase(g_last_launch.begin());
+    g_last_launch.push_back({s, decode_segments});
+    return nullptr;
+}
+
+static bool decode_overlap_enabled() {
+    int v = g_decode_overlap.load();
+    if (v < 0) {
+        const char* e = std::getenv("ADAKV_DECODE_OVERLAP");
+        v = (e && e[0] == '0') ? 0 : 1;
+        g_decode_overlap.store(v);
+    }
+    return v != 0;
+}
 
 // ---------------------------------------------------------------- errors
 namespace {
@@ -335,6 +374,7 @@ adakv_status adakv_gather(adakv_dtype dtype, const adakv_layer_shape* shape, int
     if (reserve < 0) return fail(ADAKV_INVALID_ARGUMENT, "gather: negative reserve");
     if (shape->problems == 0) return ADAKV_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    exchange_last_launch(st, nullptr);
     const int64_t G = shape->kv_groups, m = shape->window;
     ADAKV_TRY(launch_layout(budgets, shape->problems, G, m, reserve, layer_budget, layer_budgets, seg_start,
                             seqlens, st));
@@ -389,6 +429,7 @@ adakv_status adakv_compress(adakv_dtype dtype, const adakv_layer_shape* shape, c
     if (workspace_bytes < L.bytes) return fail(ADAKV_WORKSPACE_TOO_SMALL, "compress: workspace too small");
     if (s.problems == 0) return ADAKV_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    exchange_last_launch(st, nullptr);
     ADAKV_CUDA_TRY(cudaMemsetAsync(workspace, 0, 4, st));
     void* scores = group_scores ? group_scores : L.scores;
 
@@ -440,7 +481,7 @@ adakv_status adakv_decode_workspace(int64_t problems, int64_t q_heads, int64_t k
 
 adakv_status adakv_decode(adakv_dtype dtype, int64_t problems, int64_t q_heads, int64_t kv_groups,
                           int64_t head_dim, int32_t scale, const void* q, void* k_cache, void* v_cache,
-                          const int32_t* seg_start, int32_t* seqlens, int64_t max_rows, const void* k_new,
+                          int64_t cache_rows, const int32_t* seg_start, int32_t* seqlens, int64_t max_rows, const void* k_new,
                           const void* v_new, void* out, void* workspace, size_t workspace_bytes,
                           adakv_stream_t stream) {
     ADAKV_TRY(validate_dtype(dtype));
@@ -450,13 +491,23 @@ adakv_status adakv_decode(adakv_dtype dtype, int64_t problems, int64_t q_heads, 
     if ((k_new == nullptr) != (v_new == nullptr))
         return fail(ADAKV_INVALID_ARGUMENT, "append_kv: k and v must both be given");
     if (max_rows <= 0) return fail(ADAKV_INVALID_ARGUMENT, "attention_weights: empty key set");
+    if (cache_rows <= 0) return fail(ADAKV_INVALID_ARGUMENT, "decode: empty cache plane");
     const size_t need = kWsHeader + decode_workspace_bytes(problems, q_heads, kv_groups, head_dim, max_rows,
                                                            acc_size(dtype));
     if (workspace_bytes < need) return fail(ADAKV_WORKSPACE_TOO_SMALL, "decode: workspace too small");
     if (problems == 0) return ADAKV_OK;
-    return launch_decode(dtype, problems, q_heads, kv_groups, head_dim, scale, q, k_cache, v_cache, seg_start,
-                         seqlens, max_rows, k_new, v_new, out, static_cast<char*>(workspace) + kWsHeader,
-                         reinterpret_cast<cudaStream_t>(stream));
+    const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const void* prev = exchange_last_launch(st, seg_start);
+    const bool overlap = decode_overlap_enabled() && prev != nullptr && prev != seg_start;
+    return launch_decode(dtype, problems, q_heads, kv_groups, head_dim, scale, q, k_cache, v_cache, cache_rows,
+                         seg_start, seqlens, max_rows, k_new, v_new, out, static_cast<char*>(workspace) + kWsHeader,
+                         overlap, st);
+}
+
+int adakv_set_decode_overlap(int enabled) {
+    const int prev = decode_overlap_enabled() ? 1 : 0;
+    g_decode_overlap.store(enabled ? 1 : 0);
+    return prev;
 }
 
 adakv_status adakv_append_kv(adakv_dtype dtype, int64_t segments, int64_t head_dim, void* k_cache,
@@ -464,6 +515,7 @@ adakv_status adakv_append_kv(adakv_dtype dtype, int64_t segments, int64_t head_d
                              const void* v_new, adakv_stream_t stream) {
     ADAKV_TRY(validate_dtype(dtype));
     if (segments < 0) return fail(ADAKV_OUT_OF_RANGE, "append_kv: head index out of range");
+    exchange_last_launch(reinterpret_cast<cudaStream_t>(stream), nullptr);
     return launch_append(dtype, segments, head_dim, k_cache, v_cache, seg_start, seqlens, k_new, v_new,
                          reinterpret_cast<cudaStream_t>(stream));
 }

@@ -227,19 +227,19 @@ size_t decode_workspace_bytes(int64_t P, int64_t H, int64_t G, int64_t d, int64_
                             decode_tc_workspace(P, H, G, d));
 }
 
-bool decode_tc_supported(adakv_dtype dt, int64_t H, int64_t G, int64_t d, int64_t nsplit);
+bool decode_tc_supported(adakv_dtype dt, int64_t H, int64_t G, int64_t d, int64_t cache_rows);
 adakv_status launch_decode_tc(int64_t P, int64_t H, int64_t G, int32_t scale, const void* q, void* kc, void* vc,
-                              const int32_t* ss, int32_t* sl, const void* kn, const void* vn, void* out, void* ws,
-                              cudaStream_t stream);
+                              int64_t cache_rows, const int32_t* ss, int32_t* sl, const void* kn, const void* vn,
+                              void* out, bool overlap_prev, cudaStream_t stream);
 
 adakv_status launch_decode(adakv_dtype dt, int64_t P, int64_t H, int64_t G, int64_t d, int32_t scale,
-                           const void* q, void* kc, void* vc, const int32_t* ss, int32_t* sl,
+                           const void* q, void* kc, void* vc, int64_t cache_rows, const int32_t* ss, int32_t* sl,
                            int64_t max_rows, const void* kn, const void* vn, void* out, void* ws,
-                           cudaStream_t stream) {
+                           bool overlap_prev, cudaStream_t stream) {
+    if (decode_tc_supported(dt, H, G, d, cache_rows))
+        return launch_decode_tc(P, H, G, scale, q, kc, vc, cache_rows, ss, sl, kn, vn, out, overlap_prev, stream);
     int64_t chunk, nsplit;
     decode_plan(P, G, max_rows, &chunk, &nsplit);
-    if (decode_tc_supported(dt, H, G, d, nsplit))
-        return launch_decode_tc(P, H, G, scale, q, kc, vc, ss, sl, kn, vn, out, ws, stream);
     if (H / G > kMaxGroupHeads) return fail(ADAKV_UNSUPPORTED, "decode: more than 16 query heads per KV group");
     if (d > 256) return fail(ADAKV_UNSUPPORTED, "decode: head_dim > 256");
     const int J = int(ceil_div(d, 32));

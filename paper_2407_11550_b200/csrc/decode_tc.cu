@@ -4,22 +4,34 @@
 // Same contract as decode.cu (attention_weights + row_times(a, V) per head over the
 // retained cache, attention.hpp:169-196 / report.hpp:133-144, with append_kv fused).
 //
+// Data movement: every warp owns a contiguous run of 16-row blocks of its group's segment
+// and streams them through a private ring of shared-memory slots with TMA
+// (cp.async.bulk.tensor, one 4 KB box per block for K and one for V, 128-byte swizzle).
+// The copies for the first ring's worth of blocks are issued before griddepcontrol.wait,
+// so under programmatic dependent launch a layer's cache streams in while the previous
+// layer's decode is still finishing.
+//
 // Per warp, keys are consumed in blocks of 16:
 //   S  = Q K^T      two m16n8k16 n8 tiles x 8 k-steps; rows = the g heads (padded to 16);
 //   P  = exp2(S*c - m)  online softmax (block max over the 4 lanes of a row);
 //   O^T += V^T P^T  eight m16n8k16 m-tiles over d.
 // The dot products are invariant to a consistent permutation of d, so Q's and K's
-// d-columns are permuted such that each lane's B-fragment words are exactly the
-// 16-byte vectors it loads (K rows: lanes of a row read 64 contiguous bytes); V's d
-// (the MMA M dimension) is permuted so each lane loads 2 x 16 B of a row (8 lanes cover
-// 128 contiguous bytes) and un-permuted when O is written.  The S accumulator fragment
-// (row = head, cols = keys 2t, 2t+1) is exactly the P^T B-fragment of the PV MMA, so P
-// never leaves registers.  K/V are streamed once from HBM for all g heads.
+// d-columns are permuted such that each lane's B-fragment words are exactly the 16-byte
+// chunks it reads; V's d (the MMA M dimension) is permuted likewise and un-permuted when O
+// is written.  Attention is also invariant to a consistent permutation of the keys: MMA key
+// slot n of an 8-key tile reads block row kperm(n), chosen with the 128-byte swizzle so that
+// both the K reads (2 rows x 64 B per 8-lane phase) and the V reads (4 rows x 32 B) hit 32
+// distinct banks.  The S accumulator fragment (row = head, cols = keys 2t, 2t+1) is exactly
+// the P^T B-fragment of the PV MMA, so P never leaves registers.
 #include <algorithm>
+#include <cstdlib>
+#include <mutex>
+#include <utility>
 
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "tc_ptx.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -29,9 +41,28 @@ unsigned long long* dbg_buf();
 
 namespace {
 
+using namespace ptx;
+
 constexpr int kBlk = 16;
-constexpr int kMaxSplitsB = 160;   // CTAs per problem (>= SM count)
-constexpr int kMaxSegDec = 64;
+constexpr int kMaxWarps = 8;               // warps per CTA: template parameter W <= kMaxWarps
+constexpr int kMaxSlots = 3;               // ring depth per warp (runtime <= kMaxSlots; 227 KB smem)
+constexpr int kBoxBytes = kBlk * 256;      // one 16-row box of K (or V): [16 rows][2 halves][128 B]
+constexpr int kMaxCS = 16;
+
+// Split-K combine chunk sent by every CTA to each owner rank: (m, l) per head (16 floats),
+// then O for the owner's columns as [column][8 heads].
+__host__ __device__ constexpr int chunk_floats(int cs) { return 16 + ((128 + cs - 1) / cs) * 8; }
+
+// Shared memory: the split-K combine buffers, then the per-warp TMA rings.
+struct DecSmem {
+    float s_ml[kMaxWarps][8][2];                    // warp partials: (m, l) per head
+    alignas(16) float stage[kMaxCS * 16 + 1024 + kMaxCS * 8];  // CTA partial, one chunk per owner
+    alignas(16) float recv[kMaxCS * 16 + 1024 + kMaxCS * 8];   // one chunk from every rank
+    uint64_t bar[kMaxWarps][kMaxSlots];
+    uint64_t rbar;                                  // receive barrier (bulk-copy complete_tx)
+};
+constexpr size_t kRingOffset = (sizeof(DecSmem) + 1023) / 1024 * 1024;
+size_t dec_smem_bytes(int nslots, int warps) { return kRingOffset + size_t(warps) * nslots * 2 * kBoxBytes + 1024; }
 
 __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
@@ -54,28 +85,65 @@ __device__ __forceinline__ float ex2f(float x) {
     return r;
 }
 
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// shared::cluster address of the same smem offset in CTA `rank` of this cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+// shared::cta -> shared::cluster bulk copy, completing tx bytes on a (possibly remote) mbarrier
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "r"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+// byte offset of 16-byte chunk c (0..15) of block row r in a swizzled box: line = 2r + half
+__device__ __forceinline__ uint32_t box_off(int r, int c) {
+    const int line = 2 * r + (c >> 3);
+    return uint32_t(line * 128 + (((c & 7) ^ (line & 7)) << 4));
+}
+
+// key slot n (0..7) of an 8-key MMA tile -> block row (see header): n = 2t + e -> 4e | (t ^ 2e)
+__device__ __forceinline__ int kperm(int n) {
+    const int t = n >> 1, e = n & 1;
+    return (e << 2) | (t ^ (e << 1));
+}
+
 // d column held by (m-tile i, fragment row r) of the PV MMA
 __device__ __forceinline__ int v_col(int i, int r) { return (i < 4 ? 0 : 64) + 8 * (r & 7) + 2 * (i & 3) + (r >> 3); }
 
-// One thread-block cluster of CS CTAs per (problem, KV group): CTA rank r streams blocks
-// [nblk r / CS, nblk (r+1) / CS) of the group's 16-row blocks, split again over its 8 warps.
-// Warp partials (m, l, O) merge in shared memory; the CS CTA partials merge through
-// distributed shared memory (each rank finishes 1/CS of the (head, column) pairs), so the
-// split-K combine needs no global round trips, fences or atomics.  Launched with
-// programmatic dependent launch: this layer's cache streams in before griddepcontrol.wait,
-// q / k_new / v_new (produced upstream) are read after it.
-constexpr int kWarpsB = 8;
-constexpr int kThreadsB = 32 * kWarpsB;
-
-__global__ void __launch_bounds__(kThreadsB, 1)
-decode_tc_kernel(const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ k_cache,
+// One thread-block cluster of CS CTAs per (problem, KV group): CTA rank r takes blocks
+// [nblk r / CS, nblk (r+1) / CS) of the group's 16-row blocks, split again over its W warps.
+// Warp partials (m, l, O) merge in shared memory; each CTA partial is then split by output
+// column and sent with one bulk DSMEM copy per rank to the rank that finishes those columns,
+// so the split-K combine needs no global round trips, atomics or remote loads.
+template <int CS, int W>
+__global__ void __launch_bounds__(32 * W, 1)
+decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                 const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ k_cache,
                  __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ seg_start,
                  int32_t* __restrict__ seqlens, const __nv_bfloat16* __restrict__ k_new,
                  const __nv_bfloat16* __restrict__ v_new, __nv_bfloat16* __restrict__ out, int H, int G,
-                 float scale_log2, unsigned long long* __restrict__ dbg) {
+                 float scale_log2, int nslots, unsigned long long* __restrict__ dbg) {
     constexpr int d = 128;
+    extern __shared__ uint8_t smem_raw[];
+    // 1024-byte alignment by offsetting the __shared__ array itself (keeps the shared window,
+    // so every access below compiles to LDS/STS rather than generic LD/ST)
+    uint8_t* smem_al = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    DecSmem& S = *reinterpret_cast<DecSmem*>(smem_al);
+    auto ring_of = [&](int w) { return smem_al + kRingOffset + size_t(w) * nslots * 2 * kBoxBytes; };
     cg::cluster_group cluster = cg::this_cluster();
-    const int CS = int(cluster.num_blocks());
     const int rank = int(cluster.block_rank());
     const int pg = blockIdx.x / CS;
     const int p = pg / G, g = pg % G;
@@ -84,65 +152,61 @@ decode_tc_kernel(const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict_
     const int gid = lane >> 2, tig = lane & 3;
     const bool append = k_new != nullptr;
     const bool head_ok = gid < gs;
-    auto stamp = [&](int k) {
+    uint8_t* ring = ring_of(warp);  // this warp's TMA slots
+    auto stamp = [&](int k) {       // (debug) per-CTA phase timestamps
         if (dbg && threadIdx.x == 0) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-            dbg[blockIdx.x * 8 + k] = t;
+            dbg[blockIdx.x * 32 + k] = t;
+            dbg[blockIdx.x * 32 + 16 + k] = clock64();
         }
     };
-    stamp(0);
-
-    __shared__ float s_m[kWarpsB][8], s_l[kWarpsB][8];
-    __shared__ float s_o[kWarpsB][8][d];
-    __shared__ float c_m[8], c_l[8];
-    __shared__ float c_o[8][d];
-
     // this layer's own cache state (written by its previous decode step, long complete)
     const int L_old = __ldcg(seqlens + pg);
+    const int base = seg_start[pg];
+    stamp(0);
+    // rank r finishes output columns [128 r / CS, 128 (r+1) / CS) of every head
+    constexpr int chunk = chunk_floats(CS);
+    const int col_lo = (d * rank) / CS, ncols = (d * (rank + 1)) / CS - col_lo;
+    if (threadIdx.x == 0) {
+        // receive barrier: completes when every rank's chunk has landed
+        mbar_init(&S.rbar, 1);
+        mbar_fence_init();
+        mbar_arrive_expect_tx(&S.rbar, uint32_t(CS * (64 + 32 * ncols)));
+    }
+    // first phase of the cluster barrier: every CTA has started and initialised its receive
+    // barrier before any DSMEM copy (waited on before griddepcontrol.wait, off the critical path)
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+
     const int L = L_old + (append ? 1 : 0);
-    const int64_t base = seg_start[pg];
-    const __nv_bfloat16* kn = append ? k_new + int64_t(pg) * d : nullptr;
-    const __nv_bfloat16* vn = append ? v_new + int64_t(pg) * d : nullptr;
     const int nblk = (L + kBlk - 1) / kBlk;
     const int c_lo = (nblk * rank) / CS, c_hi = (nblk * (rank + 1)) / CS;
-    const int w_lo = c_lo + ((c_hi - c_lo) * warp) / kWarpsB, w_hi = c_lo + ((c_hi - c_lo) * (warp + 1)) / kWarpsB;
+    const int w_lo = c_lo + ((c_hi - c_lo) * warp) / W, w_hi = c_lo + ((c_hi - c_lo) * (warp + 1)) / W;
+    const int nb = w_hi - w_lo;
 
-    // K/V loads of one 16-row block: K rows blk+gid, blk+8+gid (4 x 16 B each), V rows
-    // blk + {2t, 2t+1, 2t+8, 2t+9} (2 x 16 B each).  The appended row (r == L_old) comes from
-    // k_new / v_new, produced upstream, so it is only read when `fresh`.
-    auto load_block = [&](int blk, bool fresh, uint4 (&kv)[2][4], uint4 (&vv)[4][2]) {
-#pragma unroll
-        for (int tl = 0; tl < 2; ++tl) {
-            const int r = blk + tl * 8 + gid;
-            const bool isnew = append && r == L_old;
-            const bool ok = r < L && (!isnew || fresh);
-            const __nv_bfloat16* row = isnew ? kn : k_cache + (base + r) * d;
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                kv[tl][i] = ok ? __ldg(reinterpret_cast<const uint4*>(row) + i * 4 + tig) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int jv = 0; jv < 4; ++jv) {
-            const int r = blk + 2 * tig + (jv & 1) + (jv >> 1) * 8;
-            const bool isnew = append && r == L_old;
-            const bool ok = r < L && (!isnew || fresh);
-            const __nv_bfloat16* row = isnew ? vn : v_cache + (base + r) * d;
-            vv[jv][0] = ok ? __ldg(reinterpret_cast<const uint4*>(row) + gid) : make_uint4(0, 0, 0, 0);
-            vv[jv][1] = ok ? __ldg(reinterpret_cast<const uint4*>(row) + 8 + gid) : make_uint4(0, 0, 0, 0);
-        }
+    uint64_t* bars = S.bar[warp];
+    const uint32_t slot0 = smem_u32(ring);
+    auto issue = [&](int j) {  // lane 0: block w_lo + j into slot j % nslots
+        const int s = j % nslots;
+        const int row = base + (w_lo + j) * kBlk;
+        mbar_arrive_expect_tx(&bars[s], 2 * kBoxBytes);
+        const uint64_t pol = policy_evict_first();
+        tma_load_3d(ring + s * 2 * kBoxBytes, &tm_k, 0, 0, row, &bars[s], pol);
+        tma_load_3d(ring + s * 2 * kBoxBytes + kBoxBytes, &tm_v, 0, 0, row, &bars[s], pol);
     };
-    uint4 pkv[2][4], pvv[4][2];
-    const bool pre = w_lo < w_hi;
-    if (pre) load_block(w_lo * kBlk, false, pkv, pvv);
+    if (lane == 0) {
+        for (int s = 0; s < nslots; ++s) mbar_init(&bars[s], 1);
+        mbar_fence_init();
+        for (int j = 0; j < (nb < nslots ? nb : nslots); ++j) issue(j);
+    }
+    __syncwarp();
     stamp(1);
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     stamp(2);
-    if (pre && append && L_old >= w_lo * kBlk && L_old < (w_lo + 1) * kBlk)
-        load_block(w_lo * kBlk, true, pkv, pvv);  // the block holding the new row
 
-    // Q A-fragments for this group's heads (rows 8..15 padding)
+    // Q A-fragments for this group's heads (rows 8..15 padding); produced upstream
     uint32_t qa0[8], qa2[8];
     {
         uint4 qv[4] = {};
@@ -163,33 +227,54 @@ decode_tc_kernel(const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict_
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
 
-    for (int bi = w_lo; bi < w_hi; ++bi) {
-        const int blk = bi * kBlk;
-        uint4 kv[2][4];
-        uint4 vv[4][2];
-        if (bi == w_lo) {
-#pragma unroll
-            for (int tl = 0; tl < 2; ++tl)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) kv[tl][i] = pkv[tl][i];
-#pragma unroll
-            for (int jv = 0; jv < 4; ++jv) {
-                vv[jv][0] = pvv[jv][0];
-                vv[jv][1] = pvv[jv][1];
+    const int rk0 = kperm(gid), rk1 = 8 + kperm(gid);                // K rows of this lane (tiles 0, 1)
+    const int rv0 = kperm(2 * tig), rv1 = kperm(2 * tig + 1);         // V rows of key slots 2t, 2t+1 (+8)
+    for (int j = 0; j < nb; ++j) {
+        const int s = j % nslots;
+        const int blk = (w_lo + j) * kBlk;
+        const uint32_t ks = slot0 + uint32_t(s * 2 * kBoxBytes), vs = ks + kBoxBytes;
+        mbar_wait(&bars[s], uint32_t((j / nslots) & 1));
+        if (blk + kBlk > L_old) {
+            // the block holding the end of the segment: the appended row (produced upstream)
+            // replaces what TMA fetched at L_old; rows past it are zeroed (V must be finite)
+            for (int rr = (L_old > blk ? L_old - blk : 0); rr < kBlk; ++rr) {
+                const bool isnew = append && blk + rr == L_old;
+                const int c = lane & 15;
+                const __nv_bfloat16* src = lane < 16 ? k_new : v_new;
+                const uint4 val = isnew ? reinterpret_cast<const uint4*>(src + int64_t(pg) * d)[c] : make_uint4(0, 0, 0, 0);
+                sts128((lane < 16 ? ks : vs) + box_off(rr, c), val);
             }
-        } else {
-            load_block(blk, true, kv, vv);
+            __syncwarp();
         }
-        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+        uint4 kv[2][4], vv[4][2];
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
-            const uint4 w0v = kv[0][s >> 1], w1v = kv[1][s >> 1];
-            mma16816(s0, qa0[s], 0u, qa2[s], 0u, (s & 1) ? w0v.z : w0v.x, (s & 1) ? w0v.w : w0v.y);
-            mma16816(s1, qa0[s], 0u, qa2[s], 0u, (s & 1) ? w1v.z : w1v.x, (s & 1) ? w1v.w : w1v.y);
+        for (int i = 0; i < 4; ++i) {
+            kv[0][i] = lds128(ks + box_off(rk0, i * 4 + tig));
+            kv[1][i] = lds128(ks + box_off(rk1, i * 4 + tig));
         }
-        const int kb = blk + 2 * tig;
-        const float x0 = kb < L ? s0[0] : -INFINITY, x1 = kb + 1 < L ? s0[1] : -INFINITY;
-        const float x2 = kb + 8 < L ? s1[0] : -INFINITY, x3 = kb + 9 < L ? s1[1] : -INFINITY;
+        vv[0][0] = lds128(vs + box_off(rv0, gid));
+        vv[0][1] = lds128(vs + box_off(rv0, 8 + gid));
+        vv[1][0] = lds128(vs + box_off(rv1, gid));
+        vv[1][1] = lds128(vs + box_off(rv1, 8 + gid));
+        vv[2][0] = lds128(vs + box_off(8 + rv0, gid));
+        vv[2][1] = lds128(vs + box_off(8 + rv0, 8 + gid));
+        vv[3][0] = lds128(vs + box_off(8 + rv1, gid));
+        vv[3][1] = lds128(vs + box_off(8 + rv1, 8 + gid));
+
+        // S = Q K^T: two key tiles x two halves of d -> four independent 4-deep MMA chains
+        float s0a[4] = {0.f, 0.f, 0.f, 0.f}, s1a[4] = {0.f, 0.f, 0.f, 0.f};
+        float s0b[4] = {0.f, 0.f, 0.f, 0.f}, s1b[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int st = 0; st < 4; ++st) {
+            const uint4 w0a = kv[0][st >> 1], w1a = kv[1][st >> 1];
+            const uint4 w0b = kv[0][2 + (st >> 1)], w1b = kv[1][2 + (st >> 1)];
+            mma16816(s0a, qa0[st], 0u, qa2[st], 0u, (st & 1) ? w0a.z : w0a.x, (st & 1) ? w0a.w : w0a.y);
+            mma16816(s1a, qa0[st], 0u, qa2[st], 0u, (st & 1) ? w1a.z : w1a.x, (st & 1) ? w1a.w : w1a.y);
+            mma16816(s0b, qa0[4 + st], 0u, qa2[4 + st], 0u, (st & 1) ? w0b.z : w0b.x, (st & 1) ? w0b.w : w0b.y);
+            mma16816(s1b, qa0[4 + st], 0u, qa2[4 + st], 0u, (st & 1) ? w1b.z : w1b.x, (st & 1) ? w1b.w : w1b.y);
+        }
+        const float x0 = blk + rv0 < L ? s0a[0] + s0b[0] : -INFINITY, x1 = blk + rv1 < L ? s0a[1] + s0b[1] : -INFINITY;
+        const float x2 = blk + 8 + rv0 < L ? s1a[0] + s1b[0] : -INFINITY, x3 = blk + 8 + rv1 < L ? s1a[1] + s1b[1] : -INFINITY;
         float bm = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3));
         bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
         bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
@@ -222,76 +307,126 @@ decode_tc_kernel(const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict_
             mma16816(acc[i], __byte_perm(r0w[wd], r1w[wd], 0x5410), __byte_perm(r0w[wd], r1w[wd], 0x7632),
                      __byte_perm(r8w[wd], r9w[wd], 0x5410), __byte_perm(r8w[wd], r9w[wd], 0x7632), b0, b1);
         }
+        __syncwarp();  // every lane's reads of slot s have been consumed
+        if (lane == 0 && j + nslots < nb) issue(j + nslots);
     }
     stamp(3);
-    // ---- warps -> CTA partial (shared memory)
+    // ---- (1) warp partial -> smem: (m, l) per head; O into the warp's idle ring in a skewed
+    // [column][8 heads] layout (8 words of padding per 8 columns, so the lanes' float2 (ha, hb)
+    // stores cover 32 distinct banks per half-warp)
+    auto so_idx = [](int c, int h) { return c * 8 + 8 * (c >> 3) + h; };
     {
+        float* s_o = reinterpret_cast<float*>(ring);
         float lsum = l_run + __shfl_xor_sync(0xffffffffu, l_run, 1);
         lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
         if (tig == 0) {
-            s_m[warp][gid] = m_run;
-            s_l[warp][gid] = lsum;
+            S.s_ml[warp][gid][0] = m_run;
+            S.s_ml[warp][gid][1] = lsum;
         }
-        const int ha = 2 * tig, hb = 2 * tig + 1;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const int c0 = v_col(i, gid), c1 = v_col(i, gid + 8);
-            s_o[warp][ha][c0] = acc[i][0];
-            s_o[warp][hb][c0] = acc[i][1];
-            s_o[warp][ha][c1] = acc[i][2];
-            s_o[warp][hb][c1] = acc[i][3];
+            const int c0 = v_col(i, gid);  // v_col(i, gid + 8) == c0 + 1
+            *reinterpret_cast<float2*>(&s_o[so_idx(c0, 2 * tig)]) = make_float2(acc[i][0], acc[i][1]);
+            *reinterpret_cast<float2*>(&s_o[so_idx(c0 + 1, 2 * tig)]) = make_float2(acc[i][2], acc[i][3]);
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < gs * d; i += kThreadsB) {
-        const int h = i / d, c = i % d;
+    stamp(4);
+    // ---- (2) CTA merge of the W warp partials: thread -> (column c, head quad hq); the result
+    // (relative to the CTA max) goes to the staging chunk of the rank owning column c
+    {
+        const int nq = (gs + 3) >> 2;
+        for (int t = threadIdx.x; t < 128 * nq; t += 32 * W) {
+            const int c = t / nq, hq = t % nq;
+            float M[4], Lh[4];
+            float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int jh = 0; jh < 4; ++jh) {
+                M[jh] = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < W; ++w) M[jh] = fmaxf(M[jh], S.s_ml[w][4 * hq + jh][0]);
+                Lh[jh] = 0.f;
+            }
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                float f[4];
+#pragma unroll
+                for (int jh = 0; jh < 4; ++jh) {
+                    const float m = S.s_ml[w][4 * hq + jh][0];
+                    f[jh] = m == -INFINITY ? 0.f : ex2f(m - M[jh]);
+                    Lh[jh] += S.s_ml[w][4 * hq + jh][1] * f[jh];
+                }
+                const float4 o = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(ring_of(w)) + so_idx(c, 4 * hq));
+                O.x += o.x * f[0];
+                O.y += o.y * f[1];
+                O.z += o.z * f[2];
+                O.w += o.w * f[3];
+            }
+            const int owner = ((c + 1) * CS - 1) / d, cl = c - (d * owner) / CS;
+            float* ch = S.stage + owner * chunk;
+            *reinterpret_cast<float4*>(ch + 16 + cl * 8 + 4 * hq) = O;
+            if (cl == 0) {
+                *reinterpret_cast<float4*>(ch + 8 * hq) = make_float4(M[0], Lh[0], M[1], Lh[1]);
+                *reinterpret_cast<float4*>(ch + 8 * hq + 4) = make_float4(M[2], Lh[2], M[3], Lh[3]);
+            }
+        }
+    }
+    fence_async_smem();  // staging writes -> visible to the bulk copies (async proxy)
+    __syncthreads();
+    stamp(5);
+    // ---- (3) one bulk DSMEM copy per owner rank, completing on the owner's receive barrier
+    if (threadIdx.x < CS) {
+        const int o = threadIdx.x;
+        const int nc_o = (d * (o + 1)) / CS - (d * o) / CS;
+        bulk_s2cluster(mapa(smem_u32(S.recv + rank * chunk), o), smem_u32(S.stage + o * chunk), uint32_t(64 + 32 * nc_o),
+                       mapa(smem_u32(&S.rbar), o));
+    }
+    mbar_wait(&S.rbar, 0);
+    stamp(6);
+    // ---- (4) this rank's columns: merge the CS chunks
+    for (int t = threadIdx.x; t < ncols * gs; t += 32 * W) {
+        const int cl = t / gs, h = t % gs;
         float M = -INFINITY;
 #pragma unroll
-        for (int w = 0; w < kWarpsB; ++w) M = fmaxf(M, s_m[w][h]);
+        for (int r = 0; r < CS; ++r) M = fmaxf(M, S.recv[r * chunk + 2 * h]);
         float Ls = 0.f, Os = 0.f;
 #pragma unroll
-        for (int w = 0; w < kWarpsB; ++w) {
-            if (s_m[w][h] == -INFINITY) continue;
-            const float f = ex2f(s_m[w][h] - M);
-            Ls += s_l[w][h] * f;
-            Os += s_o[w][h][c] * f;
+        for (int r = 0; r < CS; ++r) {
+            const float* ch = S.recv + r * chunk;
+            const float mr = ch[2 * h];
+            const float f = mr == -INFINITY ? 0.f : ex2f(mr - M);
+            Ls += ch[2 * h + 1] * f;
+            Os += ch[16 + cl * 8 + h] * f;
         }
-        c_o[h][c] = Os;
-        if (c == 0) {
-            c_m[h] = M;
-            c_l[h] = Ls;
-        }
+        out[(int64_t(p) * H + g * gs + h) * d + col_lo + cl] = __float2bfloat16_rn(Os / Ls);
     }
-    cluster.sync();
-    stamp(4);
-    // ---- CTA partials -> output through DSMEM; rank r finishes pairs [512 r / CS, 512 (r+1) / CS)
-    {
-        const int npairs = gs * d;
-        const int i0 = (npairs * rank) / CS, i1 = (npairs * (rank + 1)) / CS;
-        for (int i = i0 + int(threadIdx.x); i < i1; i += kThreadsB) {
-            const int h = i / d, c = i % d;
-            float M = -INFINITY;
-            for (int r = 0; r < CS; ++r) M = fmaxf(M, *cluster.map_shared_rank(&c_m[h], r));
-            float Ls = 0.f, Os = 0.f;
-            for (int r = 0; r < CS; ++r) {
-                const float mr = *cluster.map_shared_rank(&c_m[h], r);
-                if (mr == -INFINITY) continue;
-                const float f = ex2f(mr - M);
-                Ls += *cluster.map_shared_rank(&c_l[h], r) * f;
-                Os += *cluster.map_shared_rank(&c_o[h][c], r) * f;
-            }
-            out[(int64_t(p) * H + g * gs + h) * d + c] = __float2bfloat16_rn(Os / Ls);
+    // every rank read seqlens and its rows before sending its chunk, and rank 0 has them all
+    if (rank == 0 && append) {
+        if (threadIdx.x < 32) {  // K5 append: the new row lands after the window rows
+            const __nv_bfloat16* kn = k_new + int64_t(pg) * d;
+            const __nv_bfloat16* vn = v_new + int64_t(pg) * d;
+            reinterpret_cast<uint2*>(k_cache + (int64_t(base) + L_old) * d)[threadIdx.x] = reinterpret_cast<const uint2*>(kn)[threadIdx.x];
+            reinterpret_cast<uint2*>(v_cache + (int64_t(base) + L_old) * d)[threadIdx.x] = reinterpret_cast<const uint2*>(vn)[threadIdx.x];
         }
+        if (threadIdx.x == 0) seqlens[pg] = L;
     }
-    if (rank == 0) {
-        if (append && threadIdx.x < 32) {  // K5 append: the new row lands after the window rows
-            reinterpret_cast<uint2*>(k_cache + (base + L_old) * d)[threadIdx.x] = reinterpret_cast<const uint2*>(kn)[threadIdx.x];
-            reinterpret_cast<uint2*>(v_cache + (base + L_old) * d)[threadIdx.x] = reinterpret_cast<const uint2*>(vn)[threadIdx.x];
-        }
-    }
-    cluster.sync();  // every rank has read its peers' partials and seqlens
-    if (rank == 0 && threadIdx.x == 0 && append) seqlens[pg] = L;
     stamp(7);
+}
+
+// 3-D view of a cache plane [rows][2 halves][64 bf16] with a {64, 2, 16} box (one 16-row
+// block, 4 KB) and 128-byte swizzle; rows past the plane read as zeros.
+adakv_status make_cache_map(CUtensorMap* m, const void* plane, int64_t rows) {
+    EncodeFn enc = get_encode();
+    if (!enc) return fail(ADAKV_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[3] = {64, 2, cuuint64_t(rows)};
+    const cuuint64_t strides[2] = {128, 256};
+    const cuuint32_t box[3] = {64, 2, kBlk};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(plane), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(ADAKV_CUDA_ERROR, "cuTensorMapEncodeTiled failed (decode cache plane)");
+    return ADAKV_OK;
 }
 
 }  // namespace
@@ -301,23 +436,64 @@ static unsigned long long* g_dbg = nullptr;
 unsigned long long* dbg_buf() { return g_dbg; }
 extern "C" void adakv_debug_set_decode_timestamps(void* buf) { g_dbg = static_cast<unsigned long long*>(buf); }
 
-bool decode_tc_supported(adakv_dtype dt, int64_t H, int64_t G, int64_t d, int64_t /*nsplit*/) {
-    return dt == ADAKV_BF16 && d == 128 && G > 0 && H % G == 0 && H / G <= 8;
+bool decode_tc_supported(adakv_dtype dt, int64_t H, int64_t G, int64_t d, int64_t cache_rows) {
+    return dt == ADAKV_BF16 && d == 128 && G > 0 && H % G == 0 && H / G <= 8 && cache_rows < (int64_t(1) << 31) &&
+           get_encode() != nullptr;
 }
 
-// CTAs per cluster (one cluster per (problem, group)): the largest power of two <= 16 for
-// which every cluster of the launch is co-resident (cudaOccupancyMaxActiveClusters), so no
-// cluster waits for another to drain.
+constexpr int kWarpsDec = 8;
+static int decode_warps() { return kWarpsDec; }
+
+using DecodeKernel = decltype(&decode_tc_kernel<1, kWarpsDec>);
+template <int... CS>
+static DecodeKernel kernel_for_impl(int64_t cs, std::integer_sequence<int, CS...>) {
+    DecodeKernel k = nullptr;
+    ((cs == CS + 1 ? (k = decode_tc_kernel<CS + 1, kWarpsDec>, 0) : 0), ...);
+    return k;
+}
+static DecodeKernel kernel_for(int64_t cs) { return kernel_for_impl(cs, std::make_integer_sequence<int, kMaxCS>{}); }
+
+static adakv_status prepare_kernel() {
+    static std::once_flag once;
+    static cudaError_t err = cudaSuccess;
+    std::call_once(once, [] {
+        for (int64_t cs = 1; cs <= kMaxCS && err == cudaSuccess; ++cs) {
+            err = cudaFuncSetAttribute(kernel_for(cs), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (err == cudaSuccess)
+                err = cudaFuncSetAttribute(kernel_for(cs), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(dec_smem_bytes(kMaxSlots, decode_warps())));
+        }
+    });
+    if (err != cudaSuccess) return fail(ADAKV_CUDA_ERROR, cudaGetErrorString(err));
+    return ADAKV_OK;
+}
+
+// TMA ring depth per warp (ADAKV_DECODE_SLOTS overrides; 1..kMaxSlots)
+static int decode_slots() {
+    static int n = [] {
+        const char* e = std::getenv("ADAKV_DECODE_SLOTS");
+        const int v = e ? std::atoi(e) : kMaxSlots;
+        return v < 1 ? 1 : v > kMaxSlots ? kMaxSlots : v;
+    }();
+    return n;
+}
+
+// CTAs per cluster (one cluster per (problem, group)), from cudaOccupancyMaxActiveClusters;
+// ADAKV_DECODE_CS overrides.
 int64_t decode_tc_cluster(int64_t P, int64_t G) {
+    static std::mutex mu;
     static int64_t cached_segs = -1, cached_cs = 1;
+    std::lock_guard<std::mutex> lock(mu);
     const int64_t segs = std::max<int64_t>(1, P * G);
     if (segs == cached_segs) return cached_cs;
-    cudaFuncSetAttribute(decode_tc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    int64_t best = 1;
-    for (int64_t cs = 16; cs >= 2; cs /= 2) {
+    if (prepare_kernel() != ADAKV_OK) return 1;
+    // active clusters the device can hold for each size
+    int64_t fit[kMaxCS + 1] = {};
+    for (int64_t cs = 2; cs <= kMaxCS; ++cs) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(unsigned(segs * cs));
-        cfg.blockDim = dim3(kThreadsB);
+        cfg.blockDim = dim3(32 * decode_warps());
+        cfg.dynamicSmemBytes = dec_smem_bytes(decode_slots(), decode_warps());
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = unsigned(cs);
@@ -326,11 +502,18 @@ int64_t decode_tc_cluster(int64_t P, int64_t G) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, decode_tc_kernel, &cfg) == cudaSuccess && n >= segs) {
-            best = cs;
-            break;
-        }
+        if (cudaOccupancyMaxActiveClusters(&n, kernel_for(cs), &cfg) == cudaSuccess) fit[cs] = n;
         cudaGetLastError();
+    }
+    // The largest size for which every cluster of one launch is co-resident.  (Sizing for two
+    // co-resident launches, so the next layer's clusters all start early, measured slower:
+    // the smaller clusters cost more in the combine than the earlier start saves.)
+    int64_t best = 1;
+    for (int64_t cs = kMaxCS; cs >= 2 && best == 1; --cs)
+        if (fit[cs] >= segs) best = cs;
+    if (const char* e = std::getenv("ADAKV_DECODE_CS")) {
+        const int64_t v = std::atoi(e);
+        if (v >= 1 && v <= kMaxCS) best = v;
     }
     cached_segs = segs;
     cached_cs = best;
@@ -342,18 +525,35 @@ size_t decode_tc_workspace(int64_t, int64_t, int64_t, int64_t) { return 256; }
 extern "C" int adakv_debug_decode_cluster(int64_t P, int64_t G) { return int(decode_tc_cluster(P, G)); }
 
 adakv_status launch_decode_tc(int64_t P, int64_t H, int64_t G, int32_t scale, const void* q, void* kc, void* vc,
-                              const int32_t* ss, int32_t* sl, const void* kn, const void* vn, void* out, void*,
-                              cudaStream_t stream) {
+                              int64_t cache_rows, const int32_t* ss, int32_t* sl, const void* kn, const void* vn,
+                              void* out, bool overlap_prev, cudaStream_t stream) {
+    ADAKV_TRY(prepare_kernel());
+    // tensor maps of the two planes (one pair serves every layer of a model-wide plane)
+    static std::mutex mu;
+    static const void* c_k = nullptr;
+    static const void* c_v = nullptr;
+    static int64_t c_rows = -1;
+    static CUtensorMap c_tk, c_tv;
+    CUtensorMap tk, tv;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (kc != c_k || vc != c_v || cache_rows != c_rows) {
+            ADAKV_TRY(make_cache_map(&c_tk, kc, cache_rows));
+            ADAKV_TRY(make_cache_map(&c_tv, vc, cache_rows));
+            c_k = kc;
+            c_v = vc;
+            c_rows = cache_rows;
+        }
+        tk = c_tk;
+        tv = c_tv;
+    }
     const float sc = (scale ? 1.0f / sqrtf(128.f) : 1.0f) * 1.4426950408889634f;
     const int64_t cs = decode_tc_cluster(P, G);
-    static bool attr_set = false;
-    if (!attr_set) {
-        ADAKV_CUDA_TRY(cudaFuncSetAttribute(decode_tc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr_set = true;
-    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(P * G * cs));
-    cfg.blockDim = dim3(kThreadsB);
+    cfg.blockDim = dim3(32 * decode_warps());
+    const int nslots = decode_slots();
+    cfg.dynamicSmemBytes = dec_smem_bytes(nslots, decode_warps());
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -363,11 +563,11 @@ adakv_status launch_decode_tc(int64_t P, int64_t H, int64_t G, int32_t scale, co
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
-    ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, decode_tc_kernel, static_cast<const __nv_bfloat16*>(q),
+    cfg.numAttrs = overlap_prev ? 2 : 1;
+    ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel_for(cs), tk, tv, static_cast<const __nv_bfloat16*>(q),
                                       static_cast<__nv_bfloat16*>(kc), static_cast<__nv_bfloat16*>(vc), ss, sl,
                                       static_cast<const __nv_bfloat16*>(kn), static_cast<const __nv_bfloat16*>(vn),
-                                      static_cast<__nv_bfloat16*>(out), int(H), int(G), sc, dbg_buf()));
+                                      static_cast<__nv_bfloat16*>(out), int(H), int(G), sc, nslots, dbg_buf()));
     return ADAKV_OK;
 }
 

@@ -518,26 +518,9 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
 }
 
 // ------------------------------------------------------------------ host side
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeFn get_encode() {
-    static EncodeFn fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult qr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
-            qr == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeFn>(p);
-    });
-    return fn;
-}
-
 // 3-D bf16 tensor [outer][rows][128] with a {64, 128, 1} box, 128-byte swizzle.
 adakv_status make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t outer) {
-    EncodeFn enc = get_encode();
+    ptx::EncodeFn enc = ptx::get_encode();
     if (!enc) return fail(ADAKV_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
     const cuuint64_t dims[3] = {128, rows, outer};
     const cuuint64_t strides[2] = {128 * 2, rows * 128 * 2};
@@ -592,7 +575,7 @@ bool score_window_tc_supported(adakv_dtype dt, const adakv_layer_shape& s, int64
     const int64_t gs = s.kv_groups > 0 ? s.q_heads / s.kv_groups : 0;
     return dt == ADAKV_BF16 && s.head_dim == 128 && s.window == 32 && gs >= 1 && gs * s.window <= 128 &&
            (pool_kernel == 1 || pool_kernel == 3 || pool_kernel == 5 || pool_kernel == 7) && s.outside >= 1 &&
-           s.outside + s.window < (int64_t(1) << 31) && get_encode() != nullptr;
+           s.outside + s.window < (int64_t(1) << 31) && ptx::get_encode() != nullptr;
 }
 
 size_t score_window_tc_workspace(const adakv_layer_shape& s) {

@@ -243,6 +243,7 @@ def decode(q: torch.Tensor, cache: CompressedCache, k_new: torch.Tensor | None =
     if ws is None:
         ws = workspace(decode_workspace_bytes(P, H, cache.G, d, mr), q.device, "decode")
     L.check(lib.adakv_decode(_dt(q), P, H, cache.G, d, int(bool(scale)), _p(q), _p(cache.k), _p(cache.v),
+                             cache.k.shape[0],
                              _p(cache.seg_start), _p(cache.seqlens), mr, _p(k_new), _p(v_new), _p(out), _p(ws),
                              ws.numel(), _stream()))
     return out

@@ -73,7 +73,7 @@ class DecodeGraph:
             seg = l * B * G
             L.check(self._lib.adakv_decode(
                 self._dt, B, H, G, d, self.scale, C.c_void_p(self.q[l].data_ptr()), C.c_void_p(c.k.data_ptr()),
-                C.c_void_p(c.v.data_ptr()), C.c_void_p(c.seg_start.data_ptr() + 4 * seg),
+                C.c_void_p(c.v.data_ptr()), c.k.shape[0], C.c_void_p(c.seg_start.data_ptr() + 4 * seg),
                 C.c_void_p(c.seqlens.data_ptr() + 4 * seg), self.max_rows, C.c_void_p(self.k_new[l].data_ptr()),
                 C.c_void_p(self.v_new[l].data_ptr()), C.c_void_p(self.out[l].data_ptr()),
                 C.c_void_p(self.ws.data_ptr()), self.ws.numel(), st))

@@ -100,7 +100,7 @@ def main():
         for l in range(P):
             seg = l * G
             A._lib.check(L.adakv_decode(2, 1, H, G, d, 1, C.c_void_p(dg.q[l].data_ptr()), C.c_void_p(cache.k.data_ptr()),
-                                        C.c_void_p(cache.v.data_ptr()), C.c_void_p(cache.seg_start.data_ptr() + 4 * seg),
+                                        C.c_void_p(cache.v.data_ptr()), cache.k.shape[0], C.c_void_p(cache.seg_start.data_ptr() + 4 * seg),
                                         C.c_void_p(cache.seqlens.data_ptr() + 4 * seg), max_rows, None, None,
                                         C.c_void_p(dg.out[l].data_ptr()), C.c_void_p(dg.ws.data_ptr()), dg.ws.numel(),
                                         stream))
