@@ -391,11 +391,19 @@ def run_ours(args, cfg):
     score_gbs = score_bytes / (sm_ * 1e-3) / 1e9
     dec_launch_us = dm * 1e3 / (S * L)
     dec_bytes_launch = bytes_d / (S * L)
+    traffic = {}
+    tf = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tf):
+        with open(tf) as f:
+            traffic = json.load(f)
     if dm >= sm_:
+        t = traffic.get("decode_tc_kernel")
         roof = {"kernel": "adakv decode_kernel (split-K varlen flash-decode + append)", "bound": "hbm",
                 "achieved": round(dec_bytes_launch / (dec_launch_us * 1e-6) / 1e9, 3), "peak": peak, "unit": "GB/s",
-                "frac": round(dec_bytes_launch / (dec_launch_us * 1e-6) / 1e9 / peak, 4), "traffic": None,
-                "per_launch_bytes": int(dec_bytes_launch), "avg_launch_us": round(dec_launch_us, 3)}
+                "frac": round(dec_bytes_launch / (dec_launch_us * 1e-6) / 1e9 / peak, 4),
+                "traffic": (t["dram_read_bytes"] + t["dram_write_bytes"]) if t else None,
+                "per_launch_bytes": int(dec_bytes_launch), "avg_launch_us": round(dec_launch_us, 3),
+                "traffic_source": "profiles/r01_traffic.json (ncu, dram bytes per launch)" if t else None}
     else:
         roof = {"kernel": "window scoring (K1)", "bound": "hbm", "achieved": round(score_gbs, 3), "peak": peak,
                 "unit": "GB/s", "frac": round(score_gbs / peak, 4), "traffic": None,
