@@ -27,6 +27,9 @@ namespace adakv_b200 {
 
 
 
+// (debug) per-CTA clock64 stamps of the select phases (ADAKV debug hook, scripts only)
+static unsigned long long* g_sel_dbg = nullptr;
+
 namespace {
 
 constexpr int kSelThreads = 1024;
@@ -95,10 +98,9 @@ __device__ __forceinline__ BinPick find_bin(const uint32_t* h, int64_t krem, int
 }
 
 template <class F>
-__global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams prm) {
+__global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams prm, unsigned long long* dbg) {
     using KT = typename KeyOf<F>::type;
     constexpr int kBits = KeyOf<F>::kBits;
-    constexpr int kPasses = kBits / 8;
     cg::cluster_group cluster = cg::this_cluster();
     const unsigned CS = cluster.num_blocks();
     const unsigned rank = cluster.block_rank();
@@ -116,6 +118,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     uint32_t* wcnt = hist0 + S * 256;                            // [kWarps][S][2]
     int64_t* wkept = reinterpret_cast<int64_t*>(wcnt + kWarps * S * 2);  // [kWarps][S]
     int64_t* weqb = wkept + kWarps * S;                                  // [kWarps][S]
+    uint32_t* wh = reinterpret_cast<uint32_t*>(weqb + kWarps * S);       // [kWarps][256] per-warp histograms
+    KT* kc = reinterpret_cast<KT*>(wh + kWarps * 256);                   // [hi - lo] cached keys
 
     __shared__ uint32_t ccnt[kMaxSeg][2];  // this CTA's (gt, eq) per segment
     __shared__ KT seg_prefix[kMaxSeg];
@@ -126,11 +130,17 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     __shared__ uint64_t b_raw[kMaxSeg], b_fin[kMaxSeg], b_caps[kMaxSeg];
     __shared__ double quotas[kMaxSeg];
     __shared__ int64_t wkept_before[kWarps];
-    __shared__ KT g_T;
+    __shared__ KT g_T, g_common;
     __shared__ int64_t g_take, g_k;
     __shared__ int any_active, have_hist0;
     __shared__ uint32_t s_err;
 
+    int nst = 0;
+    auto stamp = [&]() {
+        if (dbg && tid == 0 && nst < 32) dbg[blockIdx.x * 32 + nst] = clock64();
+        ++nst;
+    };
+    stamp();
     if (tid == 0) {
         s_err = 0;
         have_hist0 = 0;
@@ -140,40 +150,133 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         seg_gt[s] = 0;
         b_caps[s] = uint64_t(prm.off[s + 1] - prm.off[s]);
     }
+    // Every pass below re-reads this CTA's slice of keys: read the scores from global memory
+    // once, in coalesced order, and keep the order-preserving keys in shared memory.
+    const bool cached = prm.cache_keys != 0;
+    if (cached)
+        for (int64_t e = lo + tid; e < hi; e += kSelThreads) kc[e - lo] = KeyOf<F>::get(sc[e]);
+    auto key_at = [&](int64_t e) -> KT { return cached ? kc[e - lo] : KeyOf<F>::get(sc[e]); };
     __syncthreads();
+    stamp();
+
+    // Bits shared by every key of the problem are skipped: the radix digits start at the
+    // highest bit where the problem's min and max keys differ.  (Scores concentrate in a
+    // few exponent values, so a digit over the raw top byte would put most keys in a
+    // handful of bins and serialise the histogram atomics.)
+    __shared__ KT red_mm[kWarps][2];
+    __shared__ KT cta_mm[2];
+    __shared__ int s_top;
+    {
+        KT mn = ~KT(0), mx = KT(0);
+        for (int64_t e = lo + tid; e < hi; e += kSelThreads) {
+            const KT u = key_at(e);
+            mn = u < mn ? u : mn;
+            mx = u > mx ? u : mx;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const KT a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+            mn = a < mn ? a : mn;
+            mx = b > mx ? b : mx;
+        }
+        if (lane == 0) {
+            red_mm[warp][0] = mn;
+            red_mm[warp][1] = mx;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            KT a = ~KT(0), b = KT(0);
+            for (int w = 0; w < kWarps; ++w) {
+                a = red_mm[w][0] < a ? red_mm[w][0] : a;
+                b = red_mm[w][1] > b ? red_mm[w][1] : b;
+            }
+            cta_mm[0] = a;
+            cta_mm[1] = b;
+        }
+        cluster.sync();
+        if (tid == 0) {
+            KT v[2][8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                v[0][r] = unsigned(r) < CS ? cluster.map_shared_rank(cta_mm, r)[0] : ~KT(0);
+                v[1][r] = unsigned(r) < CS ? cluster.map_shared_rank(cta_mm, r)[1] : KT(0);
+            }
+            KT a = ~KT(0), b = KT(0);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                a = v[0][r] < a ? v[0][r] : a;
+                b = v[1][r] > b ? v[1][r] : b;
+            }
+            // empty problem slices leave a > b; any top works then
+            const KT x = a <= b ? (a ^ b) : KT(0);
+            s_top = x == 0 ? 0 : kBits - (kBits == 32 ? __clz(uint32_t(x)) : __clzll((long long)x));
+            g_common = a <= b ? a : KT(0);
+        }
+        __syncthreads();
+    }
+    const int top = s_top;                              // significant low bits
+    const int npass = top == 0 ? 1 : (top + 7) / 8;     // radix passes
+    auto lo_bit = [&](int pass) { const int v = top - 8 * (pass + 1); return v < 0 ? 0 : v; };
+    auto hi_mask = [&](int pass) {                     // bits above this pass's digit
+        const int hb = top - 8 * pass;
+        return hb >= kBits ? KT(0) : (~KT(0)) << hb;
+    };
+    const KT common = g_common & hi_mask(0);
 
     // One radix digit over all segments with seg_active[s] set: per-segment
     // histograms of elements matching that segment's prefix, cluster-summed into agg.
     int buf = 0;  // histogram double buffer; toggled only by a pass that used it
     auto radix_pass = [&](int pass) {
-        const int shift = kBits - 8 * (pass + 1);
-        const KT mask = pass == 0 ? KT(0) : (~KT(0)) << (kBits - 8 * pass);
+        const int shift = lo_bit(pass);
+        const KT mask = hi_mask(pass);
         uint32_t* hb = hist + buf * S * 256;
-        for (int i = tid; i < S * 256; i += kSelThreads) hb[i] = 0;
-        __syncthreads();
+        uint32_t* my = wh + warp * 256;  // this warp's private histogram (no inter-warp atomics)
         for (int s = 0; s < S; ++s) {
-            if (!seg_active[s]) continue;
             const int64_t a = max(lo, prm.off[s]), b = min(hi, prm.off[s + 1]);
+            if (!seg_active[s] || a >= b) {
+                for (int i = tid; i < 256; i += kSelThreads) hb[s * 256 + i] = 0;
+                continue;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) my[lane * 8 + i] = 0;
+            __syncwarp();
             const KT pre = seg_prefix[s];
             for (int64_t base = a; base < b; base += kSelThreads) {
                 const int64_t e = base + tid;
                 int key = -1;
                 if (e < b) {
-                    const KT u = KeyOf<F>::get(sc[e]);
+                    const KT u = key_at(e);
                     if ((u & mask) == pre) key = int((u >> shift) & 0xFF);
                 }
-                const unsigned peers = __match_any_sync(0xffffffffu, key);
-                if (key >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hb[s * 256 + key], __popc(peers));
+                if (key >= 0) atomicAdd(&my[key], 1u);  // warp-private: only intra-warp collisions
             }
+            __syncthreads();
+            if (tid < 256) {
+                uint32_t t = 0;
+#pragma unroll 8
+                for (int w = 0; w < kWarps; ++w) t += wh[w * 256 + tid];
+                hb[s * 256 + tid] = t;
+            }
+            __syncthreads();
         }
+        if (pass == 0) stamp();
         cluster.sync();
+        if (pass == 0) stamp();
+        // sum the CS histograms through DSMEM: all remote loads issued before any is used
+        // (segment s has elements only in ranks [r0, r1]: the others' histograms are zero)
         for (int i = tid; i < S * 256; i += kSelThreads) {
-            uint32_t t = 0;
-            for (unsigned r = 0; r < CS; ++r) t += cluster.map_shared_rank(hb, r)[i];
-            agg[i] = t;
+            const int sg = i >> 8;
+            const unsigned r0 = unsigned((prm.off[sg] * CS) / N);
+            const unsigned r1 = unsigned(((prm.off[sg + 1] > 0 ? prm.off[sg + 1] - 1 : 0) * CS) / N);
+            uint32_t v[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) v[r] = (unsigned(r) + r0 <= r1) ? cluster.map_shared_rank(hb, r0 + r)[i] : 0u;
+            agg[i] = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
         }
         __syncthreads();
+        if (pass == 0) stamp();
         buf ^= 1;
+        stamp();
     };
 
     // ---------------- Phase A: layer-wide top-k (Algorithm 1, budget.hpp:118-140)
@@ -183,11 +286,11 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         __shared__ KT g_prefix;
         if (tid == 0) {
             g_krem = g_k;
-            g_prefix = 0;
+            g_prefix = common;
         }
         for (int s = tid; s < S; s += kSelThreads) seg_active[s] = 1;
         __syncthreads();
-        for (int pass = 0; pass < kPasses; ++pass) {
+        for (int pass = 0; pass < npass; ++pass) {
             for (int s = tid; s < S; s += kSelThreads) seg_prefix[s] = g_prefix;
             __syncthreads();
             radix_pass(pass);
@@ -208,7 +311,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                 if (lane == 0) {
                     g_bin = bp.bin;
                     g_krem -= bp.cum_above;
-                    g_prefix |= KT(bp.bin) << (kBits - 8 * (pass + 1));
+                    g_prefix |= KT(bp.bin) << lo_bit(pass);
                 }
             }
             __syncthreads();
@@ -219,7 +322,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                 for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
                 if (lane == 0) {
                     seg_gt[s] += t;
-                    if (pass == kPasses - 1) seg_need[s] = agg[s * 256 + g_bin];  // eq_s
+                    if (pass == npass - 1) seg_need[s] = agg[s * 256 + g_bin];  // eq_s
                 }
             }
             __syncthreads();
@@ -240,6 +343,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     }
     __syncthreads();
 
+    stamp();
     // ---------------- Phase C: allocation (one thread, redundantly per CTA, bit-exact fp64)
     if (tid == 0) {
         uint32_t e = 0;
@@ -279,7 +383,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
             } else {
                 seg_mode[s] = MODE_THRESH;
                 seg_active[s] = 1;
-                seg_prefix[s] = 0;
+                seg_prefix[s] = common;
                 seg_krem[s] = b;
                 any_active = 1;
             }
@@ -295,9 +399,10 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         }
     }
 
+    stamp();
     // ---------------- Phase D: per-segment top-b (topk_decision, policies.hpp:80-93)
     if (any_active) {
-        for (int pass = 0; pass < kPasses; ++pass) {
+        for (int pass = 0; pass < npass; ++pass) {
             if (pass == 0 && have_hist0) {
                 for (int i = tid; i < S * 256; i += kSelThreads) agg[i] = hist0[i];
                 __syncthreads();
@@ -309,7 +414,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                 const BinPick bp = find_bin(agg + s * 256, seg_krem[s], lane);
                 if (lane == 0) {
                     seg_krem[s] -= bp.cum_above;
-                    seg_prefix[s] |= KT(bp.bin) << (kBits - 8 * (pass + 1));
+                    seg_prefix[s] |= KT(bp.bin) << lo_bit(pass);
                 }
             }
             __syncthreads();
@@ -322,6 +427,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     }
     __syncthreads();
 
+    stamp();
     // ---------------- Phase E: keep mask and kept positions in flat order
     const int64_t wlo = lo + (hi - lo) * warp / kWarps, whi = lo + (hi - lo) * (warp + 1) / kWarps;
     const unsigned lt = (1u << lane) - 1u;
@@ -337,7 +443,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
             for (int64_t base = a; base < b; base += 32) {
                 const int64_t e = base + lane;
                 KT u = 0;
-                if (e < b) u = KeyOf<F>::get(sc[e]);
+                if (e < b) u = key_at(e);
                 gt += __popc(__ballot_sync(0xffffffffu, e < b && u > T));
                 eq += __popc(__ballot_sync(0xffffffffu, e < b && u == T));
             }
@@ -366,7 +472,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         ccnt[s][0] = gt;
         ccnt[s][1] = eq;
     }
+    stamp();
     cluster.sync();
+    stamp();
     // cross-CTA prefix: T-equal elements and kept elements before this CTA
     __shared__ int64_t cta_kept_before;
     __shared__ int64_t seg_kept_before[kMaxSeg];
@@ -428,7 +536,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                 bool keep = false;
                 if (mode == MODE_THRESH) {
                     KT u = 0;
-                    if (valid) u = KeyOf<F>::get(sc[e]);
+                    if (valid) u = key_at(e);
                     const bool is_eq = valid && u == T;
                     const unsigned beq = __ballot_sync(0xffffffffu, is_eq);
                     const int64_t eqr = run_eq + __popc(beq & lt);
@@ -446,21 +554,29 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
             }
         }
     }
+    stamp();
     cluster.sync();  // keep peer shared memory alive until every CTA is done reading it
+    stamp();
 }
 
 }  // namespace
 
 size_t select_smem_bytes(int S) {
-    return size_t(4) * (2 * S * 256 + S * 256 + S * 256 + kWarps * S * 2) + size_t(8) * 2 * kWarps * S;
+    return size_t(4) * (2 * S * 256 + S * 256 + S * 256 + kWarps * S * 2) + size_t(8) * 2 * kWarps * S +
+           size_t(4) * kWarps * 256;
 }
+constexpr size_t kSelSmemCap = 220 * 1024;  // dynamic shared memory budget per CTA
 
 adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStream_t stream) {
     if (P == 0) return ADAKV_OK;
     const int64_t per_cta = 16384;
     int CS = int(ceil_div(prm.N, per_cta));
     CS = CS < 1 ? 1 : (CS > 8 ? 8 : CS);
-    const size_t smem = select_smem_bytes(prm.S);
+    size_t smem = select_smem_bytes(prm.S);
+    const size_t key_bytes = size_t(ceil_div(prm.N, CS)) * (key64 ? 8 : 4);
+    SelParams lp = prm;
+    lp.cache_keys = smem + key_bytes <= kSelSmemCap;
+    if (lp.cache_keys) smem += key_bytes;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(P * CS));
     cfg.blockDim = dim3(kSelThreads);
@@ -475,13 +591,15 @@ adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStre
     cfg.numAttrs = 1;
     if (key64) {
         ADAKV_CUDA_TRY(cudaFuncSetAttribute(select_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel<double>, prm));
+        ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel<double>, lp, g_sel_dbg));
     } else {
         ADAKV_CUDA_TRY(cudaFuncSetAttribute(select_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel<float>, prm));
+        ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel<float>, lp, g_sel_dbg));
     }
     return ADAKV_OK;
 }
+
+extern "C" void adakv_debug_set_select_timestamps(void* buf) { g_sel_dbg = static_cast<unsigned long long*>(buf); }
 
 // ---------------------------------------------------------------- standalone budget kernels
 __global__ void budget_kernel(int op, const double* quotas_in, const int64_t* a_in, int64_t h,

@@ -21,6 +21,7 @@ struct SelParams {
     int32_t* kept_pos;
     int64_t kept_stride;
     uint32_t* err;
+    int cache_keys;            // set by launch_select: each CTA's key slice lives in shared memory
 };
 
 adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStream_t stream);
