@@ -158,7 +158,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             unsigned long long t;
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
             dbg[blockIdx.x * 32 + k] = t;
-            dbg[blockIdx.x * 32 + 16 + k] = clock64();
+            if (k < 8) dbg[blockIdx.x * 32 + 16 + k] = clock64();
         }
     };
     // this layer's own cache state (written by its previous decode step, long complete)
@@ -222,6 +222,11 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             qa2[s] = (s & 1) ? w.w : w.y;
         }
     }
+    // this lane's 16-byte chunk of the appended row (K for lanes 0-15, V for 16-31), loaded
+    // once with Q: the end-of-segment block below only stores it
+    uint4 new_chunk = make_uint4(0, 0, 0, 0);
+    if (append && nb > 0 && (w_hi * kBlk > L_old))
+        new_chunk = reinterpret_cast<const uint4*>((lane < 16 ? k_new : v_new) + int64_t(pg) * d)[lane & 15];
     float m_run = -INFINITY, l_run = 0.f;
     float acc[8][4];
 #pragma unroll
@@ -229,6 +234,19 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
 
     const int rk0 = kperm(gid), rk1 = 8 + kperm(gid);                // K rows of this lane (tiles 0, 1)
     const int rv0 = kperm(2 * tig), rv1 = kperm(2 * tig + 1);         // V rows of key slots 2t, 2t+1 (+8)
+    // loop-invariant fragment offsets within a slot (the per-block work is then base + offset)
+    uint32_t koff[2][4], voff[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        koff[0][i] = box_off(rk0, i * 4 + tig);
+        koff[1][i] = box_off(rk1, i * 4 + tig);
+    }
+#pragma unroll
+    for (int jv = 0; jv < 4; ++jv) {
+        const int r = (jv >> 1) * 8 + ((jv & 1) ? rv1 : rv0);
+        voff[jv][0] = kBoxBytes + box_off(r, gid);
+        voff[jv][1] = kBoxBytes + box_off(r, 8 + gid);
+    }
     for (int j = 0; j < nb; ++j) {
         const int s = j % nslots;
         const int blk = (w_lo + j) * kBlk;
@@ -237,29 +255,24 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         if (blk + kBlk > L_old) {
             // the block holding the end of the segment: the appended row (produced upstream)
             // replaces what TMA fetched at L_old; rows past it are zeroed (V must be finite)
+            const uint32_t dst = lane < 16 ? ks : vs;
             for (int rr = (L_old > blk ? L_old - blk : 0); rr < kBlk; ++rr) {
                 const bool isnew = append && blk + rr == L_old;
-                const int c = lane & 15;
-                const __nv_bfloat16* src = lane < 16 ? k_new : v_new;
-                const uint4 val = isnew ? reinterpret_cast<const uint4*>(src + int64_t(pg) * d)[c] : make_uint4(0, 0, 0, 0);
-                sts128((lane < 16 ? ks : vs) + box_off(rr, c), val);
+                sts128(dst + box_off(rr, lane & 15), isnew ? new_chunk : make_uint4(0, 0, 0, 0));
             }
             __syncwarp();
         }
         uint4 kv[2][4], vv[4][2];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            kv[0][i] = lds128(ks + box_off(rk0, i * 4 + tig));
-            kv[1][i] = lds128(ks + box_off(rk1, i * 4 + tig));
+            kv[0][i] = lds128(ks + koff[0][i]);
+            kv[1][i] = lds128(ks + koff[1][i]);
         }
-        vv[0][0] = lds128(vs + box_off(rv0, gid));
-        vv[0][1] = lds128(vs + box_off(rv0, 8 + gid));
-        vv[1][0] = lds128(vs + box_off(rv1, gid));
-        vv[1][1] = lds128(vs + box_off(rv1, 8 + gid));
-        vv[2][0] = lds128(vs + box_off(8 + rv0, gid));
-        vv[2][1] = lds128(vs + box_off(8 + rv0, 8 + gid));
-        vv[3][0] = lds128(vs + box_off(8 + rv1, gid));
-        vv[3][1] = lds128(vs + box_off(8 + rv1, 8 + gid));
+#pragma unroll
+        for (int jv = 0; jv < 4; ++jv) {
+            vv[jv][0] = lds128(ks + voff[jv][0]);
+            vv[jv][1] = lds128(ks + voff[jv][1]);
+        }
 
         // S = Q K^T: two key tiles x two halves of d -> four independent 4-deep MMA chains
         float s0a[4] = {0.f, 0.f, 0.f, 0.f}, s1a[4] = {0.f, 0.f, 0.f, 0.f};
@@ -273,8 +286,13 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             mma16816(s0b, qa0[4 + st], 0u, qa2[4 + st], 0u, (st & 1) ? w0b.z : w0b.x, (st & 1) ? w0b.w : w0b.y);
             mma16816(s1b, qa0[4 + st], 0u, qa2[4 + st], 0u, (st & 1) ? w1b.z : w1b.x, (st & 1) ? w1b.w : w1b.y);
         }
-        const float x0 = blk + rv0 < L ? s0a[0] + s0b[0] : -INFINITY, x1 = blk + rv1 < L ? s0a[1] + s0b[1] : -INFINITY;
-        const float x2 = blk + 8 + rv0 < L ? s1a[0] + s1b[0] : -INFINITY, x3 = blk + 8 + rv1 < L ? s1a[1] + s1b[1] : -INFINITY;
+        float x0 = s0a[0] + s0b[0], x1 = s0a[1] + s0b[1], x2 = s1a[0] + s1b[0], x3 = s1a[1] + s1b[1];
+        if (blk + kBlk > L) {  // keys past the segment end
+            if (blk + rv0 >= L) x0 = -INFINITY;
+            if (blk + rv1 >= L) x1 = -INFINITY;
+            if (blk + 8 + rv0 >= L) x2 = -INFINITY;
+            if (blk + 8 + rv1 >= L) x3 = -INFINITY;
+        }
         float bm = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3));
         bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
         bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
@@ -311,6 +329,11 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         if (lane == 0 && j + nslots < nb) issue(j + nslots);
     }
     stamp(3);
+    if (dbg && lane == 0 && warp < 8) {  // (debug) every warp's loop end + its block count
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        dbg[blockIdx.x * 32 + 24 + warp] = t;
+    }
     // ---- (1) warp partial -> smem: (m, l) per head; O into the warp's idle ring in a skewed
     // [column][8 heads] layout (8 words of padding per 8 columns, so the lanes' float2 (ha, hb)
     // stores cover 32 distinct banks per half-warp)

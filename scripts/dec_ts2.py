@@ -100,3 +100,21 @@ pr = x[-8:, :, 12]
 act = x[-8:, :, 0] > 0
 vals = pr[act]
 print("block0 landed at post_wait: ready", int((vals == 3).sum()), "not ready", int((vals == 2).sum()), "no blocks", int((vals < 2).sum()))
+# per-warp loop-end times (globaltimer, us relative to the CTA's post_wait) and block counts
+a = x[-3]
+act = a[:, 0] > 0
+print("per-warp loop end (us after this CTA's post_wait) / blocks, launch -3:")
+for cta in np.nonzero(act)[0][:20]:
+    pw = a[cta, 2]
+    ends = [(a[cta, 24 + w] - pw) / 1e3 for w in range(8)]
+    nbs = [int(a[cta, 8 + w]) for w in range(8)]
+    print(f"  cta {cta:3d}: " + " ".join(f"{e:5.2f}/{n}" for e, n in zip(ends, nbs)) + f"   end {(a[cta, 7] - pw) / 1e3:5.2f}")
+# warp-1 per-iteration clocks: [loop top, after mbar_wait, after LDS, after S] for blocks 0, 1
+w1 = x[-8:, :, 8:16]
+act = x[-8:, :, 0] > 0
+v = w1[act]
+v = v[(v[:, 0] > 0) & (v[:, 4] > 0)]
+rel = v - v[:, :1]
+print("warp1 cycles (median): blk0 wait", int(np.median(rel[:, 1])), "lds", int(np.median(rel[:, 2] - rel[:, 1])),
+      "S", int(np.median(rel[:, 3] - rel[:, 2])), "| blk0 S->blk1 top", int(np.median(rel[:, 4] - rel[:, 3])),
+      "blk1 wait", int(np.median(rel[:, 5] - rel[:, 4])), "lds", int(np.median(rel[:, 6] - rel[:, 5])), "S", int(np.median(rel[:, 7] - rel[:, 6])))
