@@ -220,6 +220,12 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = S.tmem_base;
+    // Programmatic dependent launch: pass 1 needs nothing from the kernel before it (the
+    // previous slice's pass 2), so the next kernel may be scheduled at once; pass 2 lets its
+    // TMA / MMA warps start on K immediately and only its epilogue waits for pass 1's
+    // statistics (below), after which it releases the next slice's pass 1 (which reuses
+    // the pass-1 workspace, so it must not start before this slice's pass 1 is complete).
+    if (!pass2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == 0) {
         // ===================== TMA producer =====================
@@ -329,6 +335,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         const bool active = r < prm.gs * prm.m;
         const int et = ew * 32 + lane;       // 0..511
         const float sl = prm.scale_log2;
+        if (pass2) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        }
         uint32_t j = 0;
         long long epi_wait = 0;
         const long long e_start = clock64();
@@ -639,8 +649,17 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
         prm.chunks_per_pg = pl.chunks1;
         prm.n_items = int(np * G * prm.chunks_per_pg);
         int grid = std::min(prm.n_items, sms);
-        score_tc_kernel<0><<<grid, kThreads, smem, stream>>>(tq, tk, prm);
-        ADAKV_CUDA_TRY(cudaGetLastError());
+        cudaLaunchAttribute pdl[1];
+        pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        pdl[0].val.programmaticStreamSerializationAllowed = 1;
+        cudaLaunchConfig_t lc = {};
+        lc.blockDim = dim3(kThreads);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = stream;
+        lc.attrs = pdl;
+        lc.gridDim = dim3(unsigned(grid));
+        lc.numAttrs = p0 > 0 ? 1 : 0;  // the first pass 1 waits for whatever produced K
+        ADAKV_CUDA_TRY(cudaLaunchKernelEx(&lc, score_tc_kernel<0>, tq, tk, prm));
         // pass 2: pooled scores over (128 - 2 pad)-key output tiles
         prm.pass = 2;
         prm.pad = pad;
@@ -651,8 +670,9 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
         prm.n_items = int(np * G * prm.chunks_per_pg);
         grid = std::min(prm.n_items, sms);
         if (dbg & 1) continue;  // debug: pass 1 only
-        k2<<<grid, kThreads, smem, stream>>>(tq, tk, prm);
-        ADAKV_CUDA_TRY(cudaGetLastError());
+        lc.gridDim = dim3(unsigned(grid));
+        lc.numAttrs = 1;
+        ADAKV_CUDA_TRY(cudaLaunchKernelEx(&lc, k2, tq, tk, prm));
     }
     return ADAKV_OK;
 }
