@@ -241,15 +241,32 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
             for (int i = 0; i < 8; ++i) my[lane * 8 + i] = 0;
             __syncwarp();
             const KT pre = seg_prefix[s];
-            for (int64_t base = a; base < b; base += kSelThreads) {
-                const int64_t e = base + tid;
-                int key = -1;
-                if (e < b) {
-                    const KT u = key_at(e);
-                    if ((u & mask) == pre) key = int((u >> shift) & 0xFF);
+            if (cached) {
+                // 16-byte vector reads of the cached keys: V consecutive keys per thread
+                constexpr int V = 16 / int(sizeof(KT));
+                const int64_t a0 = a - lo, b0 = b - lo;
+                for (int64_t base = (a0 / V) * V + int64_t(tid) * V; base < b0; base += int64_t(kSelThreads) * V) {
+                    const uint4 raw = *reinterpret_cast<const uint4*>(kc + base);
+                    const KT* kk = reinterpret_cast<const KT*>(&raw);
+#pragma unroll
+                    for (int i = 0; i < V; ++i) {
+                        const KT u = kk[i];
+                        if (base + i >= a0 && base + i < b0 && (u & mask) == pre)
+                            atomicAdd(&my[int((u >> shift) & 0xFF)], 1u);  // warp-private histogram
+                    }
                 }
-                if (key >= 0) atomicAdd(&my[key], 1u);  // warp-private: only intra-warp collisions
+            } else {
+                for (int64_t base = a; base < b; base += kSelThreads) {
+                    const int64_t e = base + tid;
+                    int key = -1;
+                    if (e < b) {
+                        const KT u = key_at(e);
+                        if ((u & mask) == pre) key = int((u >> shift) & 0xFF);
+                    }
+                    if (key >= 0) atomicAdd(&my[key], 1u);  // warp-private: only intra-warp collisions
+                }
             }
+            if (pass == 1) stamp();
             __syncthreads();
             if (tid < 256) {
                 uint32_t t = 0;
@@ -259,9 +276,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
             }
             __syncthreads();
         }
-        if (pass == 0) stamp();
+        if (pass == 1) stamp();
         cluster.sync();
-        if (pass == 0) stamp();
+        if (pass == 1) stamp();
         // sum the CS histograms through DSMEM: all remote loads issued before any is used
         // (segment s has elements only in ranks [r0, r1]: the others' histograms are zero)
         for (int i = tid; i < S * 256; i += kSelThreads) {
@@ -274,7 +291,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
             agg[i] = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
         }
         __syncthreads();
-        if (pass == 0) stamp();
+        if (pass == 1) stamp();
         buf ^= 1;
         stamp();
     };
@@ -573,7 +590,7 @@ adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStre
     int CS = int(ceil_div(prm.N, per_cta));
     CS = CS < 1 ? 1 : (CS > 8 ? 8 : CS);
     size_t smem = select_smem_bytes(prm.S);
-    const size_t key_bytes = size_t(ceil_div(prm.N, CS)) * (key64 ? 8 : 4);
+    const size_t key_bytes = size_t(ceil_div(prm.N, CS)) * (key64 ? 8 : 4) + 16;  // + vector-read slack
     SelParams lp = prm;
     lp.cache_keys = smem + key_bytes <= kSelSmemCap;
     if (lp.cache_keys) smem += key_bytes;
