@@ -37,6 +37,14 @@ class OutOfRange(AdaKVError, IndexError):
     pass
 
 
+class FormatError(AdaKVError):
+    """Malformed or unsupported on-disk content (serde.hpp:18-21)."""
+
+
+class IoError(AdaKVError, OSError):
+    """Underlying I/O failure (serde.hpp:24-27)."""
+
+
 class PolicyConfig(C.Structure):
     _fields_ = [("kind", C.c_int32), ("scale", C.c_int32), ("window_size", C.c_int64),
                 ("pool_kernel", C.c_int64), ("alpha", C.c_double), ("sink_tokens", C.c_int64),
@@ -112,4 +120,8 @@ def check(status: int) -> None:
             raise InvalidArgument(status, msg)
         if status == 2:
             raise OutOfRange(status, msg)
+        if status == 3:
+            raise FormatError(status, msg)
+        if status == 4:
+            raise IoError(status, msg)
         raise AdaKVError(status, msg)
