@@ -240,6 +240,12 @@ adakv_status adakv_append_kv(adakv_dtype dtype, int64_t segments, int64_t head_d
                              void* k_cache, void* v_cache, const int32_t* seg_start,
                              int32_t* seqlens, const void* k_new, const void* v_new,
                              adakv_stream_t stream);
+/* append_kv (attention.hpp:126-134) repeated `rows` times per segment (e.g. the question
+ * tokens appended after a question-agnostic compression): k_new / v_new DEVICE
+ * [segments, rows, d]; seqlens[s] += rows.  Requires seqlens + rows <= capacity. */
+adakv_status adakv_append_rows(adakv_dtype dtype, int64_t segments, int64_t rows, int64_t head_dim,
+                               void* k_cache, void* v_cache, const int32_t* seg_start, int32_t* seqlens,
+                               const void* k_new, const void* v_new, adakv_stream_t stream);
 
 /* ----------------------------------------------------------------------------
  * Budget integerisation on the device (bit-exact fp64, no FMA contraction).

@@ -6,10 +6,10 @@ Python host side: ctypes bindings (_lib), torch-tensor ops (ops), the model-leve
 pipeline (pipeline) and multi-GPU sharding (sharding).
 """
 from ._lib import AdaKVError, InvalidArgument, OutOfRange, lib  # noqa: F401
-from .ops import (CompressedCache, append_kv, apportion, compress, decode,  # noqa: F401
+from .ops import (CompressedCache, append_kv, append_rows, apportion, compress, decode,  # noqa: F401
                   pyramid_layer_budgets, repair_zero_budgets, safeguard_blend, segmented_select,
                   uniform_allocation, window_scores, workspace_status)
 
 __all__ = ["AdaKVError", "InvalidArgument", "OutOfRange", "CompressedCache", "compress", "decode",
-           "append_kv", "window_scores", "segmented_select", "apportion", "uniform_allocation",
+           "append_kv", "append_rows", "window_scores", "segmented_select", "apportion", "uniform_allocation",
            "safeguard_blend", "repair_zero_budgets", "pyramid_layer_budgets", "workspace_status", "lib"]

@@ -94,6 +94,7 @@ def _sig(L):
     L.adakv_decode.argtypes = [S, I64, I64, I64, I64, I32, VP, VP, VP, I64, VP, VP, I64, VP, VP, VP, VP, SZ, VP]
     L.adakv_decode_workspace.argtypes = [I64, I64, I64, I64, I64, PSZ]
     L.adakv_append_kv.argtypes = [S, I64, I64, VP, VP, VP, VP, VP, VP, VP]
+    L.adakv_append_rows.argtypes = [S, I64, I64, I64, VP, VP, VP, VP, VP, VP, VP]
     L.adakv_apportion.argtypes = [VP, I64, I64, VP, VP]
     L.adakv_uniform_allocation.argtypes = [I64, I64, VP, VP]
     L.adakv_safeguard_blend.argtypes = [VP, I64, I64, I64, C.c_double, VP, VP]

@@ -37,7 +37,7 @@ adakv_status launch_decode(adakv_dtype dt, int64_t P, int64_t H, int64_t G, int6
                            const void* q, void* kc, void* vc, int64_t cache_rows, const int32_t* ss, int32_t* sl,
                            int64_t max_rows, const void* kn, const void* vn, void* out, void* ws,
                            bool overlap_prev, cudaStream_t stream);
-adakv_status launch_append(adakv_dtype dt, int64_t segments, int64_t d, void* kc, void* vc,
+adakv_status launch_append(adakv_dtype dt, int64_t segments, int64_t rows, int64_t d, void* kc, void* vc,
                            const int32_t* ss, int32_t* sl, const void* kn, const void* vn,
                            cudaStream_t stream);
 __global__ void budget_kernel(int op, const double* quotas_in, const int64_t* a_in, int64_t h,
@@ -516,7 +516,20 @@ adakv_status adakv_append_kv(adakv_dtype dtype, int64_t segments, int64_t head_d
     ADAKV_TRY(validate_dtype(dtype));
     if (segments < 0) return fail(ADAKV_OUT_OF_RANGE, "append_kv: head index out of range");
     exchange_last_launch(reinterpret_cast<cudaStream_t>(stream), nullptr);
-    return launch_append(dtype, segments, head_dim, k_cache, v_cache, seg_start, seqlens, k_new, v_new,
+    return launch_append(dtype, segments, 1, head_dim, k_cache, v_cache, seg_start, seqlens, k_new, v_new,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+adakv_status adakv_append_rows(adakv_dtype dtype, int64_t segments, int64_t rows, int64_t head_dim,
+                               void* k_cache, void* v_cache, const int32_t* seg_start, int32_t* seqlens,
+                               const void* k_new, const void* v_new, adakv_stream_t stream) {
+    ADAKV_TRY(validate_dtype(dtype));
+    if (segments < 0) return fail(ADAKV_OUT_OF_RANGE, "append_kv: head index out of range");
+    if (rows < 0) return fail(ADAKV_INVALID_ARGUMENT, "append_kv: negative row count");
+    if ((k_new == nullptr || v_new == nullptr) && rows > 0 && segments > 0)
+        return fail(ADAKV_INVALID_ARGUMENT, "append_kv: k and v must both be given");
+    exchange_last_launch(reinterpret_cast<cudaStream_t>(stream), nullptr);
+    return launch_append(dtype, segments, rows, head_dim, k_cache, v_cache, seg_start, seqlens, k_new, v_new,
                          reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -163,19 +163,21 @@ decode_kernel(const T* __restrict__ q, T* __restrict__ k_cache, T* __restrict__ 
     }
 }
 
-__global__ void append_kernel(int64_t segments, int64_t d, const int32_t* __restrict__ seg_start,
+// append_kv (attention.hpp:126-134), `rows` rows per segment: block s appends
+// new[s, 0..rows) after the segment's current end and advances seqlens[s] by rows.
+__global__ void append_kernel(int64_t segments, int64_t rows, int64_t d, const int32_t* __restrict__ seg_start,
                               int32_t* __restrict__ seqlens, const uint16_t* __restrict__ kn,
                               const uint16_t* __restrict__ vn, uint16_t* __restrict__ kc,
                               uint16_t* __restrict__ vc, int64_t esz_units) {
     const int64_t s = blockIdx.x;
-    const int64_t row = int64_t(seg_start[s]) + seqlens[s];
+    const int64_t row0 = int64_t(seg_start[s]) + seqlens[s];
     const int64_t w = d * esz_units;  // row width in 16-bit units
-    for (int64_t i = threadIdx.x; i < w; i += blockDim.x) {
-        kc[row * w + i] = kn[s * w + i];
-        vc[row * w + i] = vn[s * w + i];
+    for (int64_t i = threadIdx.x; i < rows * w; i += blockDim.x) {
+        kc[row0 * w + i] = kn[s * rows * w + i];
+        vc[row0 * w + i] = vn[s * rows * w + i];
     }
     __syncthreads();
-    if (threadIdx.x == 0) seqlens[s] += 1;
+    if (threadIdx.x == 0) seqlens[s] += int32_t(rows);
 }
 
 template <class T, int J, int GH>
@@ -271,13 +273,13 @@ adakv_status launch_decode(adakv_dtype dt, int64_t P, int64_t H, int64_t G, int6
     return fail(ADAKV_INVALID_ARGUMENT, "decode: unknown dtype");
 }
 
-adakv_status launch_append(adakv_dtype dt, int64_t segments, int64_t d, void* kc, void* vc,
+adakv_status launch_append(adakv_dtype dt, int64_t segments, int64_t rows, int64_t d, void* kc, void* vc,
                            const int32_t* ss, int32_t* sl, const void* kn, const void* vn,
                            cudaStream_t stream) {
-    if (segments == 0) return ADAKV_OK;
+    if (segments == 0 || rows == 0) return ADAKV_OK;
     const int64_t units = int64_t(dtype_size(dt)) / 2;
     append_kernel<<<unsigned(segments), 128, 0, stream>>>(
-        segments, d, ss, sl, static_cast<const uint16_t*>(kn), static_cast<const uint16_t*>(vn),
+        segments, rows, d, ss, sl, static_cast<const uint16_t*>(kn), static_cast<const uint16_t*>(vn),
         static_cast<uint16_t*>(kc), static_cast<uint16_t*>(vc), units);
     ADAKV_CUDA_TRY(cudaGetLastError());
     return ADAKV_OK;

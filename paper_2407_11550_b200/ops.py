@@ -256,6 +256,18 @@ def append_kv(cache: CompressedCache, k_new: torch.Tensor, v_new: torch.Tensor) 
                                     _p(cache.seg_start), _p(cache.seqlens), _p(k_new), _p(v_new), _stream()))
 
 
+def append_rows(cache: CompressedCache, k_new: torch.Tensor, v_new: torch.Tensor) -> None:
+    """append_kv (attention.hpp:126-134) of T rows per segment: k_new/v_new [P*G, T, d] (e.g. the
+    question tokens after a question-agnostic compression).  The cache needs T spare rows per
+    segment (compress(..., reserve >= T + decode steps))."""
+    _need_cuda(k_new, v_new)
+    S, T, d = k_new.shape
+    if S != cache.P * cache.G or d != cache.d or v_new.shape != k_new.shape:
+        raise L.InvalidArgument(1, "append_kv: row shape mismatch")
+    L.check(L.lib().adakv_append_rows(_dt(k_new), S, T, d, _p(cache.k), _p(cache.v), _p(cache.seg_start),
+                                      _p(cache.seqlens), _p(k_new.contiguous()), _p(v_new.contiguous()), _stream()))
+
+
 # ---------------------------------------------------------------- budget helpers (device fp64)
 def _i64(x):
     return np.ascontiguousarray(np.asarray(x, dtype=np.int64))

@@ -30,6 +30,32 @@ def compress_model(q, k, v, layer_budget, *, kind="ada_snapkv", pool_kernel=7, a
                         sink_tokens=sink_tokens, reserve=reserve, layer_budgets=layer_budgets, out=out, ws=ws)
 
 
+def pyramid_problem_budgets(avg_outside_per_layer, layers, batch, G, m, beta_max=1.5, beta_min=0.5, device=None):
+    """Per-problem layer budgets for compress_model under the pyramid kinds: the linear
+    schedule of pyramid_layer_budgets (budget.hpp:169-191) over the layers' OUTSIDE budgets,
+    plus the m*G window entries, repeated for every request (problems are layer-major)."""
+    sched = ops.pyramid_layer_budgets(int(avg_outside_per_layer), int(layers), float(beta_max), float(beta_min))
+    lb = torch.as_tensor(sched, dtype=torch.int64).repeat_interleave(int(batch)) + int(m) * int(G)
+    return lb.to(device) if device is not None else lb
+
+
+def compress_question_agnostic(q_ctx, k_ctx, v_ctx, layer_budget, k_question, v_question, *,
+                               kind="ada_snapkv", pool_kernel=7, alpha=0.2, reserve=0, layer_budgets=None):
+    """Question-agnostic compression (config 5): the observation window is the
+    last m tokens of the CONTEXT (q_ctx = their queries, [L, B, H, m, d]); the context cache
+    is compressed first and the question tokens' K/V ([L, B, G, T, d]) are appended afterwards
+    with one append_kv of T rows per segment.  `reserve` must cover T plus the decode steps."""
+    Lyr, B = q_ctx.shape[:2]
+    T = k_question.shape[3]
+    if reserve < T:
+        raise L.InvalidArgument(1, "compress_question_agnostic: reserve must cover the question tokens")
+    cache = compress_model(q_ctx, k_ctx, v_ctx, layer_budget, kind=kind, pool_kernel=pool_kernel, alpha=alpha,
+                           reserve=reserve, layer_budgets=layer_budgets)
+    G, d = k_question.shape[2], k_question.shape[4]
+    ops.append_rows(cache, k_question.reshape(Lyr * B * G, T, d), v_question.reshape(Lyr * B * G, T, d))
+    return cache
+
+
 class DecodeGraph:
     """One decode step over all layers, captured as a CUDA graph.
 

@@ -353,3 +353,46 @@ def test_device_error_latch(dev):
     r = A.segmented_select(s, [0, 5, 10], 0, "given", budgets=torch.tensor([[6, 1]], dtype=torch.int32, device=dev))
     with pytest.raises(A.InvalidArgument):
         A.workspace_status(r["ws"])
+
+
+# --------------------------------------------------------------------------- question-agnostic glue
+def test_question_agnostic_append_then_decode(dev, oracle_mod):
+    """Config-5 flow: compress on the context window, append T question rows per segment with
+    adakv_append_rows (bit-exact copies after the window rows), then decode over the result."""
+    from paper_2407_11550_b200 import pipeline as PL
+    O = oracle_mod
+    Lyr, B, H, G, m, n_o, d, T = 2, 2, 32, 8, 32, 2016, 128, 16
+    q, k, v = planted_layer(Lyr * B, H, G, n_o, m, d, seed=23, dtype=torch.bfloat16, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(5)
+    kq = torch.randn((Lyr, B, G, T, d), generator=gen, device=dev).to(torch.bfloat16)
+    vq = torch.randn((Lyr, B, G, T, d), generator=gen, device=dev).to(torch.bfloat16)
+    LB = 256 * G
+    cache = PL.compress_question_agnostic(q.view(Lyr, B, H, m, d), k.view(Lyr, B, G, n_o + m, d),
+                                          v.view(Lyr, B, G, n_o + m, d), LB, kq, vq, reserve=T + 4)
+    plain = A.compress(q, k, v, LB, reserve=T + 4)
+    budgets = plain.budgets.cpu().numpy()
+    for p in range(Lyr * B):
+        for g in range(G):
+            kr, vr = cache.segment(p, g)
+            k0, v0 = plain.segment(p, g)
+            assert kr.shape[0] == int(budgets[p * G + g]) + m + T
+            assert torch.equal(kr[:-T], k0) and torch.equal(vr[:-T], v0)
+            assert torch.equal(kr[-T:], kq.view(-1, G, T, d)[p, g]) and torch.equal(vr[-T:], vq.view(-1, G, T, d)[p, g])
+    qd = torch.randn((Lyr * B, H, d), generator=gen, device=dev).to(torch.bfloat16)
+    o = A.decode(qd, cache)
+    for p in (0, 3):
+        segs = [cache.segment(p, g) for g in range(G)]
+        off = np.concatenate([[0], np.cumsum([s[0].shape[0] for s in segs])])
+        ref = O.decode_attention(qd[p].double().cpu().numpy(), torch.cat([s[0] for s in segs]).double().cpu().numpy(),
+                                 torch.cat([s[1] for s in segs]).double().cpu().numpy(), off)
+        err = np.abs(o[p].double().cpu().numpy() - ref).max()
+        assert err <= 2e-2, err
+
+
+def test_pyramid_problem_budgets_layer_major(dev, oracle_mod):
+    from paper_2407_11550_b200 import pipeline as PL
+    O = oracle_mod
+    lb = PL.pyramid_problem_budgets(1000, 4, 3, G=8, m=32)
+    sched = O.pyramid_layer_budgets(1000, 4, 1.5, 0.5)
+    assert lb.tolist() == [int(x) + 256 for x in np.repeat(sched, 3)]
