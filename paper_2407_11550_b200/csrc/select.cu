@@ -266,7 +266,6 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                     if (key >= 0) atomicAdd(&my[key], 1u);  // warp-private: only intra-warp collisions
                 }
             }
-            if (pass == 1) stamp();
             __syncthreads();
             if (tid < 256) {
                 uint32_t t = 0;
@@ -276,9 +275,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
             }
             __syncthreads();
         }
-        if (pass == 1) stamp();
         cluster.sync();
-        if (pass == 1) stamp();
         // sum the CS histograms through DSMEM: all remote loads issued before any is used
         // (segment s has elements only in ranks [r0, r1]: the others' histograms are zero)
         for (int i = tid; i < S * 256; i += kSelThreads) {
@@ -291,7 +288,6 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
             agg[i] = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
         }
         __syncthreads();
-        if (pass == 1) stamp();
         buf ^= 1;
         stamp();
     };
