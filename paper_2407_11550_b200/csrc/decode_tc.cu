@@ -56,7 +56,6 @@ __host__ __device__ constexpr int chunk_floats(int cs) { return 16 + ((128 + cs 
 // Shared memory: the split-K combine buffers, then the per-warp TMA rings.
 struct DecSmem {
     float s_ml[kMaxWarps][8][2];                    // warp partials: (m, l) per head
-    alignas(16) float stage[kMaxCS * 16 + 1024 + kMaxCS * 8];  // CTA partial, one chunk per owner
     alignas(16) float recv[kMaxCS * 16 + 1024 + kMaxCS * 8];   // one chunk from every rank
     uint64_t bar[kMaxWarps][kMaxSlots];
     uint64_t rbar;                                  // receive barrier (bulk-copy complete_tx)
@@ -101,13 +100,12 @@ __device__ __forceinline__ uint32_t mapa(uint32_t addr, int rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
     return r;
 }
-// shared::cta -> shared::cluster bulk copy, completing tx bytes on a (possibly remote) mbarrier
-__device__ __forceinline__ void bulk_s2cluster(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
-    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "r"(src), "r"(bytes), "r"(bar)
+// 16-byte store into (possibly remote) cluster shared memory, completing tx bytes on its mbarrier
+__device__ __forceinline__ void st_async_v4(uint32_t addr, float4 v, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1,%2,%3,%4}, [%5];" ::"r"(addr),
+                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(bar)
                  : "memory");
 }
-
 // byte offset of 16-byte chunk c (0..15) of block row r in a swizzled box: line = 2r + half
 __device__ __forceinline__ uint32_t box_off(int r, int c) {
     const int line = 2 * r + (c >> 3);
@@ -172,7 +170,8 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         // receive barrier: completes when every rank's chunk has landed
         mbar_init(&S.rbar, 1);
         mbar_fence_init();
-        mbar_arrive_expect_tx(&S.rbar, uint32_t(CS * (64 + 32 * ncols)));
+        const int nq = (gs + 3) >> 2;  // head quads: each (column, quad) arrives as one 16-byte store
+        mbar_arrive_expect_tx(&S.rbar, uint32_t(CS * nq * (32 + 16 * ncols)));
     }
     // first phase of the cluster barrier: every CTA has started and initialised its receive
     // barrier before any DSMEM copy (waited on before griddepcontrol.wait, off the critical path)
@@ -356,7 +355,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     __syncthreads();
     stamp(4);
     // ---- (2) CTA merge of the W warp partials: thread -> (column c, head quad hq); the result
-    // (relative to the CTA max) goes to the staging chunk of the rank owning column c
+    // (relative to the CTA max) goes to the rank owning column c
     {
         const int nq = (gs + 3) >> 2;
         for (int t = threadIdx.x; t < 128 * nq; t += 32 * W) {
@@ -386,24 +385,16 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
                 O.w += o.w * f[3];
             }
             const int owner = ((c + 1) * CS - 1) / d, cl = c - (d * owner) / CS;
-            float* ch = S.stage + owner * chunk;
-            *reinterpret_cast<float4*>(ch + 16 + cl * 8 + 4 * hq) = O;
+            // straight into the owner's receive chunk for this rank (DSMEM st.async)
+            const uint32_t dst = smem_u32(S.recv + rank * chunk), bar = mapa(smem_u32(&S.rbar), owner);
+            st_async_v4(mapa(dst + 4u * uint32_t(16 + cl * 8 + 4 * hq), owner), O, bar);
             if (cl == 0) {
-                *reinterpret_cast<float4*>(ch + 8 * hq) = make_float4(M[0], Lh[0], M[1], Lh[1]);
-                *reinterpret_cast<float4*>(ch + 8 * hq + 4) = make_float4(M[2], Lh[2], M[3], Lh[3]);
+                st_async_v4(mapa(dst + 4u * uint32_t(8 * hq), owner), make_float4(M[0], Lh[0], M[1], Lh[1]), bar);
+                st_async_v4(mapa(dst + 4u * uint32_t(8 * hq + 4), owner), make_float4(M[2], Lh[2], M[3], Lh[3]), bar);
             }
         }
     }
-    fence_async_smem();  // staging writes -> visible to the bulk copies (async proxy)
-    __syncthreads();
     stamp(5);
-    // ---- (3) one bulk DSMEM copy per owner rank, completing on the owner's receive barrier
-    if (threadIdx.x < CS) {
-        const int o = threadIdx.x;
-        const int nc_o = (d * (o + 1)) / CS - (d * o) / CS;
-        bulk_s2cluster(mapa(smem_u32(S.recv + rank * chunk), o), smem_u32(S.stage + o * chunk), uint32_t(64 + 32 * nc_o),
-                       mapa(smem_u32(&S.rbar), o));
-    }
     mbar_wait(&S.rbar, 0);
     stamp(6);
     // ---- (4) this rank's columns: merge the CS chunks
