@@ -408,7 +408,11 @@ def run_ours(args, cfg):
         roof = {"kernel": "window scoring (K1)", "bound": "hbm", "achieved": round(score_gbs, 3), "peak": peak,
                 "unit": "GB/s", "frac": round(score_gbs / peak, 4), "traffic": None,
                 "per_launch_bytes": int(score_bytes), "avg_launch_us": round(sm_ * 1e3, 3)}
-    launches = args.steps * (5 + S * L)
+    # our kernels per step: scoring = 2 launches per slice of problems (slices of <= 48 MB of K,
+    # score_window_tc.cu make_plan), then select + layout + gather, then S * L decode launches
+    k_bytes = G * n * d * 2
+    slice_p = max(1, min(P, (48 << 20) // k_bytes))
+    launches = args.steps * (2 * (-(-P // slice_p)) + 3 + S * L)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
         "warmup": warmups, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",

@@ -50,6 +50,10 @@ constexpr uint32_t kHalfBytes = 128 * 128;        // [128 rows][64 bf16]
 constexpr uint32_t kTileBytes = 2 * kHalfBytes;   // a [128 x 128] bf16 tile
 constexpr uint32_t kA2Bytes = 128 * 128 * 2;      // E^T tile, fp16
 constexpr float kEScaleLog2 = 16.f;               // E carries a 2^16 scale (fp16 range)
+#ifndef ADAKV_PASS2_POLY
+#define ADAKV_PASS2_POLY 0
+#endif
+constexpr int kPass2Poly = ADAKV_PASS2_POLY;      // pass-2 exp2 split (see exp2_mixed)
 
 struct __align__(1024) Smem {
     uint8_t q[2][kHalfBytes];
@@ -76,7 +80,7 @@ struct TcParams {
     int G, H, gs, m, n_o, step, pad;
     int tiles_per_pg, tiles_per_item, chunks_per_pg, n_items;
     int pg_base;
-    int debug;  // bit 1: MUFU only (no polynomial exp2); bit 2: skip the pass-1 ticket/fold
+    int debug;  // (experiments) 1: pass 1 only; 4/8/16: skip ticket / fences / fold; 64: MUFU-only exp2 in pass 1
     float scale_log2;
     float log2_m;
     float inv_g;
@@ -85,6 +89,7 @@ struct TcParams {
     unsigned* tickets;   // [pg]
     float* head_scores;  // [P][H][n_o] or null
     float* group_scores; // [P][G][n_o]
+    long long* dbg;      // (debug) per-CTA role wait counters, 16 per CTA per pass, or null
 };
 
 // ------------------------------------------------------------------ epilogue helpers
@@ -154,7 +159,8 @@ __device__ __forceinline__ void pass2_group(uint32_t taddr, int lane, int r, int
     }
     pool_inplace<PAD, NV, NOUT>(v);
 #pragma unroll
-    for (int o = 0; o < NOUT; ++o) v[o] = ex2(fmaf(v[o], sl, -lw2));
+    for (int o = 0; o < NOUT; ++o) v[o] = fmaf(v[o], sl, -lw2);
+    exp2_mixed<NV, kPass2Poly>(v, NOUT);  // of every 8, kPass2Poly on the FMA pipe, the rest on MUFU
     // E^T tile (fp16, MN-major SW128): window row r = K index, output o = M index
     mbar_wait(e_empty_bar, e_parity);
     uint8_t* rowbase = a2tile + (r >> 3) * 2048 + (CG >> 1) * 1024 + (r & 7) * 128;
@@ -260,8 +266,8 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                     }
                 }
             }
-            if (prm.debug & 32) {
-                long long* ts = reinterpret_cast<long long*>(prm.head_scores) + blockIdx.x * 8;
+            if (prm.dbg) {
+                long long* ts = prm.dbg + ((prm.pass - 1) * 160 + blockIdx.x) * 16;
                 ts[0] = prod_wait;
                 ts[1] = clock64() - p_start;
             }
@@ -273,11 +279,15 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             constexpr uint32_t idesc2 = idesc_f16_f32(128, 16, 1);
             uint32_t stage = 0, sphase = 0, qphase = 0;
             uint32_t j = 0;  // tile sequence number of this CTA
-            long long mma_wait_acc = 0, mma_wait_full = 0;
+            long long mma_wait_acc = 0, mma_wait_full = 0, mma_wait_e = 0, mma_wait_d2 = 0;
             auto mma2 = [&](uint32_t i) {
                 const uint32_t b = i & 1, ph = (i >> 1) & 1;
+                long long w = clock64();
                 mbar_wait(&S.e_full[b], ph);
+                mma_wait_e += clock64() - w;
+                w = clock64();
                 mbar_wait(&S.d2_empty[b], ph ^ 1);
+                mma_wait_d2 += clock64() - w;
                 tc_fence_after();
 #pragma unroll
                 for (int s = 0; s < 8; ++s) {
@@ -317,15 +327,20 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                         stage = 0;
                         sphase ^= 1;
                     }
-                    if (pass2 && j > 0) mma2(j - 1);
+                    // the head-sum MMA of tile j-2 (two tiles of slack: QK of the next tile is
+                    // not held back by the slowest epilogue warp of the previous one)
+                    if (pass2 && j > 1) mma2(j - 2);
                 }
                 mma_commit(&S.q_empty);
             }
+            if (pass2 && j > 1) mma2(j - 2);
             if (pass2 && j > 0) mma2(j - 1);
-            if (prm.debug & 32) {
-                long long* ts = reinterpret_cast<long long*>(prm.head_scores) + blockIdx.x * 8;
+            if (prm.dbg) {
+                long long* ts = prm.dbg + ((prm.pass - 1) * 160 + blockIdx.x) * 16;
                 ts[2] = mma_wait_acc;
                 ts[3] = mma_wait_full;
+                ts[7] = mma_wait_e;
+                ts[8] = mma_wait_d2;
             }
         }
     } else {
@@ -344,7 +359,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         uint32_t j = 0;
         long long epi_wait = 0;
         const long long e_start = clock64();
-        int prev_pg = -1, prev_t = 0;
+        int prev_pg = -1, prev_t = 0, prev2_pg = -1, prev2_t = 0;
         auto readout = [&](uint32_t i, int rpg, int rt) {
             // D2 of tile i: lanes = output keys, columns = heads (one warp per lane quarter)
             const uint32_t b = i & 1, ph = (i >> 1) & 1;
@@ -414,9 +429,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                     if (nm != -INFINITY) {
 #pragma unroll
                         for (int c = 0; c < 32; ++c) v[c] = fmaf(v[c], sl, -nm);
-                        if (prm.debug & 64) exp2_mixed<32, 2>(v, 32);
-                        else if (prm.debug & 128) exp2_mixed<32, 4>(v, 32);
-                        else exp2_mixed<32, 0>(v, 32);
+                        // 2 of every 8 exp2 on the FMA pipe (polynomial), 6 on MUFU: measured
+                        // fastest split (debug 64: MUFU only)
+                        if (prm.debug & 64) exp2_mixed<32, 0>(v, 32);
+                        else exp2_mixed<32, 2>(v, 32);
                         uint64_t a0 = pk(0.f, 0.f), a1 = pk(0.f, 0.f);
 #pragma unroll
                         for (int c = 0; c < 32; c += 4) {
@@ -443,8 +459,11 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                         default: pass2_group<PAD, 3>(taddr, lane, r, key_col0, prm.n_o, sl, lw, S.a2[eb], &S.acc_empty[ab],
                                                      &S.e_empty[eb], eph ^ 1, &S.e_full[eb]); break;
                     }
-                    // the last column group (fewest outputs) reads back the previous tile's scores
-                    if (cg == 3 && j > 0) readout(j - 1, prev_pg, prev_t);
+                    // one column group (rotating, so the extra work is spread evenly over the
+                    // epilogue warps) reads back the scores of tile j-2
+                    if (j > 1 && cg == int((j - 2) & 3)) readout(j - 2, prev2_pg, prev2_t);
+                    prev2_pg = prev_pg;
+                    prev2_t = prev_t;
                     prev_pg = pg;
                     prev_t = t;
                 }
@@ -515,9 +534,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                 }
             }
         }
-        if (pass2 && cg == 3 && j > 0) readout(j - 1, prev_pg, prev_t);
-        if ((prm.debug & 32) && et == 0) {
-            long long* ts = reinterpret_cast<long long*>(prm.head_scores) + blockIdx.x * 8;
+        if (pass2 && j > 1 && cg == int((j - 2) & 3)) readout(j - 2, prev2_pg, prev2_t);
+        if (pass2 && j > 0 && cg == int((j - 1) & 3)) readout(j - 1, prev_pg, prev_t);
+        if (prm.dbg && et == 0) {
+            long long* ts = prm.dbg + ((prm.pass - 1) * 160 + blockIdx.x) * 16;
             ts[4] = epi_wait;
             ts[5] = clock64() - e_start;
             ts[6] = j;
@@ -530,6 +550,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
 }
 
 // ------------------------------------------------------------------ host side
+long long* g_score_dbg = nullptr;  // (debug) role wait counters, scripts/tc_ts.py
 // 3-D bf16 tensor [outer][rows][128] with a {64, 128, 1} box, 128-byte swizzle.
 adakv_status make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t outer) {
     ptx::EncodeFn enc = ptx::get_encode();
@@ -642,6 +663,7 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
             return e ? std::atoi(e) : 0;
         }();
         prm.debug = dbg;
+        prm.dbg = g_score_dbg;
         // pass 1: row statistics over 128-key tiles
         prm.pass = 1;
         prm.step = kTile;
@@ -680,3 +702,7 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
 }
 
 }  // namespace adakv_b200
+
+extern "C" void adakv_debug_set_score_counters(void* buf) {
+    adakv_b200::g_score_dbg = static_cast<long long*>(buf);
+}
