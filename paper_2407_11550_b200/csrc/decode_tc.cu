@@ -44,7 +44,10 @@ namespace {
 using namespace ptx;
 
 constexpr int kBlk = 16;
-constexpr int kMaxWarps = 8;               // warps per CTA: template parameter W <= kMaxWarps
+#ifndef ADAKV_DECODE_W
+#define ADAKV_DECODE_W 8
+#endif
+constexpr int kMaxWarps = ADAKV_DECODE_W;   // warps per CTA (template parameter W <= kMaxWarps)
 constexpr int kMaxSlots = 3;               // ring depth per warp (runtime <= kMaxSlots; 227 KB smem)
 constexpr int kBoxBytes = kBlk * 256;      // one 16-row box of K (or V): [16 rows][2 halves][128 B]
 constexpr int kMaxCS = 16;
@@ -455,7 +458,7 @@ bool decode_tc_supported(adakv_dtype dt, int64_t H, int64_t G, int64_t d, int64_
            get_encode() != nullptr;
 }
 
-constexpr int kWarpsDec = 8;
+constexpr int kWarpsDec = ADAKV_DECODE_W;
 static int decode_warps() { return kWarpsDec; }
 
 using DecodeKernel = decltype(&decode_tc_kernel<1, kWarpsDec>);
@@ -467,29 +470,34 @@ static DecodeKernel kernel_for_impl(int64_t cs, std::integer_sequence<int, CS...
 }
 static DecodeKernel kernel_for(int64_t cs) { return kernel_for_impl(cs, std::make_integer_sequence<int, kMaxCS>{}); }
 
-static adakv_status prepare_kernel() {
-    static std::once_flag once;
-    static cudaError_t err = cudaSuccess;
-    std::call_once(once, [] {
-        for (int64_t cs = 1; cs <= kMaxCS && err == cudaSuccess; ++cs) {
-            err = cudaFuncSetAttribute(kernel_for(cs), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            if (err == cudaSuccess)
-                err = cudaFuncSetAttribute(kernel_for(cs), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(dec_smem_bytes(kMaxSlots, decode_warps())));
-        }
-    });
-    if (err != cudaSuccess) return fail(ADAKV_CUDA_ERROR, cudaGetErrorString(err));
-    return ADAKV_OK;
-}
-
 // TMA ring depth per warp (ADAKV_DECODE_SLOTS overrides; 1..kMaxSlots)
 static int decode_slots() {
     static int n = [] {
         const char* e = std::getenv("ADAKV_DECODE_SLOTS");
-        const int v = e ? std::atoi(e) : kMaxSlots;
-        return v < 1 ? 1 : v > kMaxSlots ? kMaxSlots : v;
+        // the rings of all warps within 227 KB of shared memory
+        int mx = kMaxSlots;
+        while (mx > 1 && dec_smem_bytes(mx, kWarpsDec) > 227 * 1024) --mx;
+        const int v = e ? std::atoi(e) : mx;
+        return v < 1 ? 1 : v > mx ? mx : v;
     }();
     return n;
+}
+
+// Function attributes are per device: set them once for every device this process uses.
+static adakv_status prepare_kernel() {
+    static std::mutex mu;
+    static uint64_t done_mask = 0;
+    int dev = 0;
+    ADAKV_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < 64 && (done_mask >> dev) & 1) return ADAKV_OK;
+    for (int64_t cs = 1; cs <= kMaxCS; ++cs) {
+        ADAKV_CUDA_TRY(cudaFuncSetAttribute(kernel_for(cs), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        ADAKV_CUDA_TRY(cudaFuncSetAttribute(kernel_for(cs), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            int(dec_smem_bytes(decode_slots(), decode_warps()))));
+    }
+    if (dev < 64) done_mask |= uint64_t(1) << dev;
+    return ADAKV_OK;
 }
 
 // CTAs per cluster (one cluster per (problem, group)), from cudaOccupancyMaxActiveClusters;
@@ -497,9 +505,12 @@ static int decode_slots() {
 int64_t decode_tc_cluster(int64_t P, int64_t G) {
     static std::mutex mu;
     static int64_t cached_segs = -1, cached_cs = 1;
+    static int cached_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(mu);
     const int64_t segs = std::max<int64_t>(1, P * G);
-    if (segs == cached_segs) return cached_cs;
+    if (segs == cached_segs && dev == cached_dev) return cached_cs;
     if (prepare_kernel() != ADAKV_OK) return 1;
     // active clusters the device can hold for each size
     int64_t fit[kMaxCS + 1] = {};
@@ -530,6 +541,7 @@ int64_t decode_tc_cluster(int64_t P, int64_t G) {
         if (v >= 1 && v <= kMaxCS) best = v;
     }
     cached_segs = segs;
+    cached_dev = dev;
     cached_cs = best;
     return best;
 }

@@ -69,11 +69,6 @@ struct __align__(1024) Smem {
     uint32_t is_last;
 };
 
-__device__ __forceinline__ uint64_t gtime() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 
 struct TcParams {
     int pass;
