@@ -396,3 +396,43 @@ def test_pyramid_problem_budgets_layer_major(dev, oracle_mod):
     lb = PL.pyramid_problem_budgets(1000, 4, 3, G=8, m=32)
     sched = O.pyramid_layer_budgets(1000, 4, 1.5, 0.5)
     assert lb.tolist() == [int(x) + 256 for x in np.repeat(sched, 3)]
+
+
+def test_decode_graph_pdl_chain_matches_serial(dev):
+    """The bench path: one CUDA graph per decode step over all layers, consecutive layers
+    overlapped by programmatic dependent launch (each layer's cache streams in before the
+    previous layer's decode has finished).  Every step's outputs and the appended caches must
+    equal the serial, non-overlapped launches bit for bit."""
+    from paper_2407_11550_b200 import pipeline as PL
+    Lyr, B, H, G, m, n_o, d = 4, 1, 32, 8, 32, 4064, 128
+    q, k, v = planted_layer(Lyr * B, H, G, n_o, m, d, seed=29, dtype=torch.bfloat16, device=dev)
+    LB = 1024 * G
+    steps = 5
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(8)
+    qs = torch.randn((steps, Lyr, B, H, d), generator=gen, device=dev).to(torch.bfloat16)
+    ks = torch.randn((steps, Lyr, B, G, d), generator=gen, device=dev).to(torch.bfloat16)
+    vs = torch.randn((steps, Lyr, B, G, d), generator=gen, device=dev).to(torch.bfloat16)
+    outs = {}
+    L = A.lib()
+    for mode in ("graph_pdl", "serial"):
+        cache = PL.compress_model(q.view(Lyr, B, H, m, d), k.view(Lyr, B, G, n_o + m, d), v.view(Lyr, B, G, n_o + m, d),
+                                  LB, reserve=steps + 1)
+        prev = L.adakv_set_decode_overlap(1 if mode == "graph_pdl" else 0)
+        try:
+            dg = PL.DecodeGraph(cache, Lyr, B, LB + steps + 1, use_graph=(mode == "graph_pdl"))
+            res = []
+            for s in range(steps):
+                dg.q.copy_(qs[s])
+                dg.k_new.copy_(ks[s])
+                dg.v_new.copy_(vs[s])
+                res.append(dg.step().clone())
+            torch.cuda.synchronize()
+        finally:
+            L.adakv_set_decode_overlap(prev)
+        segs = [torch.cat(cache.segment(p, g)) for p in range(Lyr * B) for g in range(G)]  # valid rows only
+        outs[mode] = (torch.stack(res), segs, cache.seqlens.clone())
+    a, b = outs["graph_pdl"], outs["serial"]
+    assert torch.equal(a[2], b[2])
+    assert int(a[2][0]) == int(b[2][0]) and torch.equal(a[0], b[0])
+    assert all(torch.equal(x, y) for x, y in zip(a[1], b[1]))
