@@ -298,14 +298,20 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         float bm = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3));
         bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
         bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
-        const float m_new = fmaxf(m_run, bm * scale_log2);
-        const float corr = ex2f(m_run - m_new);
+        // lazy running max: the reference moves only when a block exceeds it by more than 8
+        // (log2 units), so probabilities stay <= 2^8 and the accumulator is rescaled rarely;
+        // the first block needs no rescale (acc and l are still zero)
+        const float m_cand = fmaxf(m_run, bm * scale_log2);
+        const bool bump = m_cand > m_run + 8.f;
+        const float m_new = bump ? m_cand : m_run;
+        const float corr = bump ? ex2f(m_run - m_new) : 1.f;
+        const bool rescale = bump && m_run != -INFINITY;
         float p0 = ex2f(fmaf(x0, scale_log2, -m_new)), p1 = ex2f(fmaf(x1, scale_log2, -m_new));
         float p2 = ex2f(fmaf(x2, scale_log2, -m_new)), p3 = ex2f(fmaf(x3, scale_log2, -m_new));
         if (!head_ok) p0 = p1 = p2 = p3 = 0.f;
         l_run = l_run * corr + ((p0 + p1) + (p2 + p3));
         m_run = m_new;
-        if (__any_sync(0xffffffffu, head_ok && corr != 1.f)) {
+        if (__any_sync(0xffffffffu, head_ok && rescale)) {
             const float ca = __shfl_sync(0xffffffffu, corr, 8 * tig);
             const float cb = __shfl_sync(0xffffffffu, corr, 8 * tig + 4);
 #pragma unroll
