@@ -36,7 +36,8 @@ def planted_rows(G: int, n: int, gen: torch.Generator, frac_sparse=0.75, top_mas
                 start = lo + int(torch.randint(0, hi - lo - ln + 1, (1,), generator=gen).item())
                 spike[start:start + ln] = True
             u = torch.rand(n, generator=gen, device="cpu").to(device)
-            e = -torch.log1p(-torch.rand(n, generator=gen, device="cpu")).to(device)
+            # exponential tail; the uniform is kept off 0 so no position gets p = 0 (ln 0 = -inf)
+            e = -torch.log1p(-torch.rand(n, generator=gen, device="cpu").clamp_min(2.0 ** -24)).to(device)
             p = torch.where(spike, 0.5 + u, e)
             ss, ts = p[spike].sum(), p[~spike].sum()
             p = torch.where(spike, p * (top_mass / ss), p * ((1 - top_mass) / ts))

@@ -436,3 +436,27 @@ def test_decode_graph_pdl_chain_matches_serial(dev):
     assert torch.equal(a[2], b[2])
     assert int(a[2][0]) == int(b[2][0]) and torch.equal(a[0], b[0])
     assert all(torch.equal(x, y) for x, y in zip(a[1], b[1]))
+
+
+def test_decode_long_segments_ring_rounds(dev, oracle_mod):
+    """Segments far longer than a CTA's TMA ring (every slot refilled several times) and a
+    few decode steps with appends, against the fp64 oracle."""
+    O = oracle_mod
+    P, H, G, m, n_o, d = 1, 32, 8, 32, 32736, 128
+    q, k, v = planted_layer(P, H, G, n_o, m, d, seed=31, dtype=torch.bfloat16, device=dev)
+    LB = 16384 * G  # half of every group's keys retained: ~16K rows per segment
+    cache = A.compress(q, k, v, LB, reserve=4)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(12)
+    for step in range(3):
+        qd = torch.randn((P, H, d), generator=gen, device=dev).to(torch.bfloat16)
+        kn = torch.randn((P, G, d), generator=gen, device=dev).to(torch.bfloat16)
+        vn = torch.randn((P, G, d), generator=gen, device=dev).to(torch.bfloat16)
+        o = A.decode(qd, cache, kn, vn)
+        segs = [cache.segment(0, g) for g in range(G)]  # include the appended row
+        off = np.concatenate([[0], np.cumsum([s[0].shape[0] for s in segs])])
+        ref = O.decode_attention(qd[0].double().cpu().numpy(), torch.cat([s[0] for s in segs]).double().cpu().numpy(),
+                                 torch.cat([s[1] for s in segs]).double().cpu().numpy(), off)
+        err = np.abs(o[0].double().cpu().numpy() - ref).max()
+        assert err <= 2e-2 and err <= 1e-2 * max(np.abs(ref).max(), 1e-3) + 4e-3, (step, err)
+        assert torch.equal(segs[3][0][-1], kn[0, 3]) and torch.equal(segs[3][1][-1], vn[0, 3])
