@@ -48,7 +48,7 @@ constexpr int kBlk = 16;
 #define ADAKV_DECODE_W 8
 #endif
 constexpr int kMaxWarps = ADAKV_DECODE_W;   // warps per CTA (template parameter W <= kMaxWarps)
-constexpr int kRing = 12;                  // CTA-wide TMA ring slots of one 16-row block (K + V, 8 KB each)
+constexpr int kMaxSlots = 3;               // ring depth per warp (runtime <= kMaxSlots; 227 KB smem)
 constexpr int kBoxBytes = kBlk * 256;      // one 16-row box of K (or V): [16 rows][2 halves][128 B]
 constexpr int kMaxCS = 16;
 
@@ -60,13 +60,11 @@ __host__ __device__ constexpr int chunk_floats(int cs) { return 16 + ((128 + cs 
 struct DecSmem {
     float s_ml[kMaxWarps][8][2];                    // warp partials: (m, l) per head
     alignas(16) float recv[kMaxCS * 16 + 1024 + kMaxCS * 8];   // one chunk from every rank
-    uint64_t bar[kRing];                            // slot full barriers (TMA complete_tx)
-    int round[kRing];                               // which round of blocks a slot was last issued for
+    uint64_t bar[kMaxWarps][kMaxSlots];
     uint64_t rbar;                                  // receive barrier (bulk-copy complete_tx)
 };
 constexpr size_t kRingOffset = (sizeof(DecSmem) + 1023) / 1024 * 1024;
-// two CTAs per SM fit: 2 x (kRingOffset + 96 KB + 1 KB) <= 228 KB
-constexpr size_t kDecSmemBytes = kRingOffset + size_t(kRing) * 2 * kBoxBytes + 1024;
+size_t dec_smem_bytes(int nslots, int warps) { return kRingOffset + size_t(warps) * nslots * 2 * kBoxBytes + 1024; }
 
 __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
@@ -105,12 +103,6 @@ __device__ __forceinline__ uint32_t mapa(uint32_t addr, int rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
     return r;
 }
-// 8-byte store into (possibly remote) cluster shared memory, completing tx bytes on its mbarrier
-__device__ __forceinline__ void st_async_v2(uint32_t addr, float x, float y, uint32_t bar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1,%2}, [%3];" ::"r"(addr),
-                 "f"(x), "f"(y), "r"(bar)
-                 : "memory");
-}
 // 16-byte store into (possibly remote) cluster shared memory, completing tx bytes on its mbarrier
 __device__ __forceinline__ void st_async_v4(uint32_t addr, float4 v, uint32_t bar) {
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1,%2,%3,%4}, [%5];" ::"r"(addr),
@@ -138,20 +130,20 @@ __device__ __forceinline__ int v_col(int i, int r) { return (i < 4 ? 0 : 64) + 8
 // column and sent with one bulk DSMEM copy per rank to the rank that finishes those columns,
 // so the split-K combine needs no global round trips, atomics or remote loads.
 template <int CS, int W>
-__global__ void __launch_bounds__(32 * W, 2)
+__global__ void __launch_bounds__(32 * W, 1)
 decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                  const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ k_cache,
                  __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ seg_start,
                  int32_t* __restrict__ seqlens, const __nv_bfloat16* __restrict__ k_new,
                  const __nv_bfloat16* __restrict__ v_new, __nv_bfloat16* __restrict__ out, int H, int G,
-                 float scale_log2, unsigned long long* __restrict__ dbg) {
+                 float scale_log2, int nslots, unsigned long long* __restrict__ dbg) {
     constexpr int d = 128;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment by offsetting the __shared__ array itself (keeps the shared window,
     // so every access below compiles to LDS/STS rather than generic LD/ST)
     uint8_t* smem_al = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     DecSmem& S = *reinterpret_cast<DecSmem*>(smem_al);
-    auto slot_of = [&](int sl) { return smem_al + kRingOffset + size_t(sl) * 2 * kBoxBytes; };
+    auto ring_of = [&](int w) { return smem_al + kRingOffset + size_t(w) * nslots * 2 * kBoxBytes; };
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = int(cluster.block_rank());
     const int pg = blockIdx.x / CS;
@@ -161,6 +153,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     const int gid = lane >> 2, tig = lane & 3;
     const bool append = k_new != nullptr;
     const bool head_ok = gid < gs;
+    uint8_t* ring = ring_of(warp);  // this warp's TMA slots
     auto stamp = [&](int k) {       // (debug) per-CTA phase timestamps
         if (dbg && threadIdx.x == 0) {
             unsigned long long t;
@@ -180,8 +173,8 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         // receive barrier: completes when every rank's chunk has landed
         mbar_init(&S.rbar, 1);
         mbar_fence_init();
-        const int np = (gs + 1) >> 1;  // head pairs: (column, pair) arrives as 8 bytes, (m, l) x 2 as 16
-        mbar_arrive_expect_tx(&S.rbar, uint32_t(CS * np * (16 + 8 * ncols)));
+        const int nq = (gs + 3) >> 2;  // head quads: each (column, quad) arrives as one 16-byte store
+        mbar_arrive_expect_tx(&S.rbar, uint32_t(CS * nq * (32 + 16 * ncols)));
     }
     // first phase of the cluster barrier: every CTA has started and initialised its receive
     // barrier before any DSMEM copy (waited on before griddepcontrol.wait, off the critical path)
@@ -190,24 +183,23 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     const int L = L_old + (append ? 1 : 0);
     const int nblk = (L + kBlk - 1) / kBlk;
     const int c_lo = (nblk * rank) / CS, c_hi = (nblk * (rank + 1)) / CS;
-    const int nbc = c_hi - c_lo;  // this CTA's blocks; warp w takes CTA blocks w, w + W, ...
+    const int w_lo = c_lo + ((c_hi - c_lo) * warp) / W, w_hi = c_lo + ((c_hi - c_lo) * (warp + 1)) / W;
+    const int nb = w_hi - w_lo;
 
-    // CTA-wide ring: CTA block b lives in slot b % kRing.  The warp that consumes block b
-    // refills its slot with block b + kRing; round[] lets the consumer of a later block wait
-    // for that issue first (before it, a parity wait could match the slot's previous round).
-    auto issue = [&](int b) {
-        const int sl = b % kRing;
-        const int row = base + (c_lo + b) * kBlk;
-        S.round[sl] = b / kRing;
-        mbar_arrive_expect_tx(&S.bar[sl], 2 * kBoxBytes);
+    uint64_t* bars = S.bar[warp];
+    const uint32_t slot0 = smem_u32(ring);
+    auto issue = [&](int j) {  // lane 0: block w_lo + j into slot j % nslots
+        const int s = j % nslots;
+        const int row = base + (w_lo + j) * kBlk;
+        mbar_arrive_expect_tx(&bars[s], 2 * kBoxBytes);
         const uint64_t pol = policy_evict_first();
-        tma_load_3d(slot_of(sl), &tm_k, 0, 0, row, &S.bar[sl], pol);
-        tma_load_3d(slot_of(sl) + kBoxBytes, &tm_v, 0, 0, row, &S.bar[sl], pol);
+        tma_load_3d(ring + s * 2 * kBoxBytes, &tm_k, 0, 0, row, &bars[s], pol);
+        tma_load_3d(ring + s * 2 * kBoxBytes + kBoxBytes, &tm_v, 0, 0, row, &bars[s], pol);
     };
-    if (threadIdx.x == 0) {
-        for (int sl = 0; sl < kRing; ++sl) mbar_init(&S.bar[sl], 1);
+    if (lane == 0) {
+        for (int s = 0; s < nslots; ++s) mbar_init(&bars[s], 1);
         mbar_fence_init();
-        for (int b = 0; b < (nbc < kRing ? nbc : kRing); ++b) issue(b);
+        for (int j = 0; j < (nb < nslots ? nb : nslots); ++j) issue(j);
     }
     __syncwarp();
     stamp(1);
@@ -235,7 +227,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     // this lane's 16-byte chunk of the appended row (K for lanes 0-15, V for 16-31), loaded
     // once with Q: the end-of-segment block below only stores it
     uint4 new_chunk = make_uint4(0, 0, 0, 0);
-    if (append && nbc > 0 && c_hi * kBlk > L_old && (nbc - 1) % W == warp)
+    if (append && nb > 0 && (w_hi * kBlk > L_old))
         new_chunk = reinterpret_cast<const uint4*>((lane < 16 ? k_new : v_new) + int64_t(pg) * d)[lane & 15];
     float m_run = -INFINITY, l_run = 0.f;
     float acc[8][4];
@@ -257,16 +249,11 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         voff[jv][0] = kBoxBytes + box_off(r, gid);
         voff[jv][1] = kBoxBytes + box_off(r, 8 + gid);
     }
-    for (int b = warp; b < nbc; b += W) {
-        const int sl = b % kRing;
-        const int blk = (c_lo + b) * kBlk;
-        const uint32_t ks = smem_u32(slot_of(sl)), vs = ks + kBoxBytes;
-        // a slot's barrier parity is only unambiguous once this round has been issued (the
-        // issue happens after the previous round of the slot was consumed, i.e. completed)
-        if (b >= kRing)
-            while (*reinterpret_cast<volatile int*>(&S.round[sl]) != b / kRing) {
-            }
-        mbar_wait(&S.bar[sl], uint32_t((b / kRing) & 1));
+    for (int j = 0; j < nb; ++j) {
+        const int s = j % nslots;
+        const int blk = (w_lo + j) * kBlk;
+        const uint32_t ks = slot0 + uint32_t(s * 2 * kBoxBytes), vs = ks + kBoxBytes;
+        mbar_wait(&bars[s], uint32_t((j / nslots) & 1));
         if (blk + kBlk > L_old) {
             // the block holding the end of the segment: the appended row (produced upstream)
             // replaces what TMA fetched at L_old; rows past it are zeroed (V must be finite)
@@ -346,8 +333,8 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             mma16816(acc[i], __byte_perm(r0w[wd], r1w[wd], 0x5410), __byte_perm(r0w[wd], r1w[wd], 0x7632),
                      __byte_perm(r8w[wd], r9w[wd], 0x5410), __byte_perm(r8w[wd], r9w[wd], 0x7632), b0, b1);
         }
-        __syncwarp();  // every lane's reads of the slot have been consumed
-        if (lane == 0 && b + kRing < nbc) issue(b + kRing);
+        __syncwarp();  // every lane's reads of slot s have been consumed
+        if (lane == 0 && j + nslots < nb) issue(j + nslots);
     }
     stamp(3);
     if (dbg && lane == 0 && warp < 8) {  // (debug) every warp's loop end + its block count
@@ -355,13 +342,12 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
         dbg[blockIdx.x * 32 + 24 + warp] = t;
     }
-    __syncthreads();  // every warp is done with the ring
-    // ---- (1) warp partial -> smem: (m, l) per head; O into ring slot `warp` in a skewed
+    // ---- (1) warp partial -> smem: (m, l) per head; O into the warp's idle ring in a skewed
     // [column][8 heads] layout (8 words of padding per 8 columns, so the lanes' float2 (ha, hb)
     // stores cover 32 distinct banks per half-warp)
     auto so_idx = [](int c, int h) { return c * 8 + 8 * (c >> 3) + h; };
     {
-        float* s_o = reinterpret_cast<float*>(slot_of(warp));
+        float* s_o = reinterpret_cast<float*>(ring);
         float lsum = l_run + __shfl_xor_sync(0xffffffffu, l_run, 1);
         lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
         if (tig == 0) {
@@ -377,36 +363,44 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     }
     __syncthreads();
     stamp(4);
-    // ---- (2) CTA merge of the W warp partials: thread -> (column c, head pair hp); the result
+    // ---- (2) CTA merge of the W warp partials: thread -> (column c, head quad hq); the result
     // (relative to the CTA max) goes to the rank owning column c
     {
-        const int np = (gs + 1) >> 1;
-        for (int t = threadIdx.x; t < 128 * np; t += 32 * W) {
-            const int c = t / np, hp = t % np;
-            float M[2] = {-INFINITY, -INFINITY}, Lh[2] = {0.f, 0.f};
+        const int nq = (gs + 3) >> 2;
+        for (int t = threadIdx.x; t < 128 * nq; t += 32 * W) {
+            const int c = t / nq, hq = t % nq;
+            float M[4], Lh[4];
+            float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int w = 0; w < W; ++w) {
-                M[0] = fmaxf(M[0], S.s_ml[w][2 * hp][0]);
-                M[1] = fmaxf(M[1], S.s_ml[w][2 * hp + 1][0]);
+            for (int jh = 0; jh < 4; ++jh) {
+                M[jh] = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < W; ++w) M[jh] = fmaxf(M[jh], S.s_ml[w][4 * hq + jh][0]);
+                Lh[jh] = 0.f;
             }
-            float2 O = make_float2(0.f, 0.f);
 #pragma unroll
             for (int w = 0; w < W; ++w) {
-                const float m0 = S.s_ml[w][2 * hp][0], m1 = S.s_ml[w][2 * hp + 1][0];
-                const float f0 = m0 == -INFINITY ? 0.f : ex2f(m0 - M[0]);
-                const float f1 = m1 == -INFINITY ? 0.f : ex2f(m1 - M[1]);
-                Lh[0] += S.s_ml[w][2 * hp][1] * f0;
-                Lh[1] += S.s_ml[w][2 * hp + 1][1] * f1;
-                const float2 o = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(slot_of(w)) + so_idx(c, 2 * hp));
-                O.x += o.x * f0;
-                O.y += o.y * f1;
+                float f[4];
+#pragma unroll
+                for (int jh = 0; jh < 4; ++jh) {
+                    const float m = S.s_ml[w][4 * hq + jh][0];
+                    f[jh] = m == -INFINITY ? 0.f : ex2f(m - M[jh]);
+                    Lh[jh] += S.s_ml[w][4 * hq + jh][1] * f[jh];
+                }
+                const float4 o = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(ring_of(w)) + so_idx(c, 4 * hq));
+                O.x += o.x * f[0];
+                O.y += o.y * f[1];
+                O.z += o.z * f[2];
+                O.w += o.w * f[3];
             }
             const int owner = ((c + 1) * CS - 1) / d, cl = c - (d * owner) / CS;
             // straight into the owner's receive chunk for this rank (DSMEM st.async)
             const uint32_t dst = smem_u32(S.recv + rank * chunk), bar = mapa(smem_u32(&S.rbar), owner);
-            st_async_v2(mapa(dst + 4u * uint32_t(16 + cl * 8 + 2 * hp), owner), O.x, O.y, bar);
-            if (cl == 0)
-                st_async_v4(mapa(dst + 4u * uint32_t(4 * hp), owner), make_float4(M[0], Lh[0], M[1], Lh[1]), bar);
+            st_async_v4(mapa(dst + 4u * uint32_t(16 + cl * 8 + 4 * hq), owner), O, bar);
+            if (cl == 0) {
+                st_async_v4(mapa(dst + 4u * uint32_t(8 * hq), owner), make_float4(M[0], Lh[0], M[1], Lh[1]), bar);
+                st_async_v4(mapa(dst + 4u * uint32_t(8 * hq + 4), owner), make_float4(M[2], Lh[2], M[3], Lh[3]), bar);
+            }
         }
     }
     stamp(5);
@@ -482,6 +476,19 @@ static DecodeKernel kernel_for_impl(int64_t cs, std::integer_sequence<int, CS...
 }
 static DecodeKernel kernel_for(int64_t cs) { return kernel_for_impl(cs, std::make_integer_sequence<int, kMaxCS>{}); }
 
+// TMA ring depth per warp (ADAKV_DECODE_SLOTS overrides; 1..kMaxSlots)
+static int decode_slots() {
+    static int n = [] {
+        const char* e = std::getenv("ADAKV_DECODE_SLOTS");
+        // the rings of all warps within 227 KB of shared memory
+        int mx = kMaxSlots;
+        while (mx > 1 && dec_smem_bytes(mx, kWarpsDec) > 227 * 1024) --mx;
+        const int v = e ? std::atoi(e) : mx;
+        return v < 1 ? 1 : v > mx ? mx : v;
+    }();
+    return n;
+}
+
 // Function attributes are per device: set them once for every device this process uses.
 static adakv_status prepare_kernel() {
     static std::mutex mu;
@@ -493,7 +500,7 @@ static adakv_status prepare_kernel() {
     for (int64_t cs = 1; cs <= kMaxCS; ++cs) {
         ADAKV_CUDA_TRY(cudaFuncSetAttribute(kernel_for(cs), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         ADAKV_CUDA_TRY(cudaFuncSetAttribute(kernel_for(cs), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            int(kDecSmemBytes)));
+                                            int(dec_smem_bytes(decode_slots(), decode_warps()))));
     }
     if (dev < 64) done_mask |= uint64_t(1) << dev;
     return ADAKV_OK;
@@ -517,7 +524,7 @@ int64_t decode_tc_cluster(int64_t P, int64_t G) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(unsigned(segs * cs));
         cfg.blockDim = dim3(32 * decode_warps());
-        cfg.dynamicSmemBytes = kDecSmemBytes;
+        cfg.dynamicSmemBytes = dec_smem_bytes(decode_slots(), decode_warps());
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = unsigned(cs);
@@ -529,12 +536,11 @@ int64_t decode_tc_cluster(int64_t P, int64_t G) {
         if (cudaOccupancyMaxActiveClusters(&n, kernel_for(cs), &cfg) == cudaSuccess) fit[cs] = n;
         cudaGetLastError();
     }
-    // The largest size <= kPreferCS for which every cluster of one launch is co-resident.
-    // Two CTAs fit per SM, so consecutive launches overlap at any size; 10 measured best at
-    // Llama-3.1-8B decode shapes (8 groups: 4.15 us vs 4.34 at 16, 4.37 at 8, scripts/dec_ts2.py).
-    constexpr int64_t kPreferCS = 10;
+    // The largest size for which every cluster of one launch is co-resident.  (Sizing for two
+    // co-resident launches, so the next layer's clusters all start early, measured slower:
+    // the smaller clusters cost more in the combine than the earlier start saves.)
     int64_t best = 1;
-    for (int64_t cs = kPreferCS; cs >= 2 && best == 1; --cs)
+    for (int64_t cs = kMaxCS; cs >= 2 && best == 1; --cs)
         if (fit[cs] >= segs) best = cs;
     if (const char* e = std::getenv("ADAKV_DECODE_CS")) {
         const int64_t v = std::atoi(e);
@@ -578,7 +584,8 @@ adakv_status launch_decode_tc(int64_t P, int64_t H, int64_t G, int32_t scale, co
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(P * G * cs));
     cfg.blockDim = dim3(32 * decode_warps());
-    cfg.dynamicSmemBytes = kDecSmemBytes;
+    const int nslots = decode_slots();
+    cfg.dynamicSmemBytes = dec_smem_bytes(nslots, decode_warps());
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -592,7 +599,7 @@ adakv_status launch_decode_tc(int64_t P, int64_t H, int64_t G, int32_t scale, co
     ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel_for(cs), tk, tv, static_cast<const __nv_bfloat16*>(q),
                                       static_cast<__nv_bfloat16*>(kc), static_cast<__nv_bfloat16*>(vc), ss, sl,
                                       static_cast<const __nv_bfloat16*>(kn), static_cast<const __nv_bfloat16*>(vn),
-                                      static_cast<__nv_bfloat16*>(out), int(H), int(G), sc, dbg_buf()));
+                                      static_cast<__nv_bfloat16*>(out), int(H), int(G), sc, nslots, dbg_buf()));
     return ADAKV_OK;
 }
 
