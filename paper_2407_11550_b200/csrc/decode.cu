@@ -234,10 +234,19 @@ adakv_status launch_decode_tc(int64_t P, int64_t H, int64_t G, int32_t scale, co
                               int64_t cache_rows, const int32_t* ss, int32_t* sl, const void* kn, const void* vn,
                               void* out, bool overlap_prev, cudaStream_t stream);
 
+bool decode_umma_enabled();
+bool decode_umma_supported(adakv_dtype dt, int64_t P, int64_t H, int64_t G, int64_t d, int64_t max_rows,
+                           int64_t cache_rows);
+adakv_status launch_decode_umma(int64_t P, int64_t H, int64_t G, int32_t scale, const void* q, void* kc, void* vc,
+                                int64_t cache_rows, const int32_t* ss, int32_t* sl, const void* kn, const void* vn,
+                                void* out, bool overlap_prev, cudaStream_t stream);
+
 adakv_status launch_decode(adakv_dtype dt, int64_t P, int64_t H, int64_t G, int64_t d, int32_t scale,
                            const void* q, void* kc, void* vc, int64_t cache_rows, const int32_t* ss, int32_t* sl,
                            int64_t max_rows, const void* kn, const void* vn, void* out, void* ws,
                            bool overlap_prev, cudaStream_t stream) {
+    if (decode_umma_enabled() && decode_umma_supported(dt, P, H, G, d, max_rows, cache_rows))
+        return launch_decode_umma(P, H, G, scale, q, kc, vc, cache_rows, ss, sl, kn, vn, out, overlap_prev, stream);
     if (decode_tc_supported(dt, H, G, d, cache_rows))
         return launch_decode_tc(P, H, G, scale, q, kc, vc, cache_rows, ss, sl, kn, vn, out, overlap_prev, stream);
     int64_t chunk, nsplit;
