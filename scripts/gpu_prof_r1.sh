@@ -1,6 +1,6 @@
 CMD="python bench.py --layers 2 --decode-steps 16 --steps 1 --warmup 3 --no-cpu-baseline"
 timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_r1.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "launch list $?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches_r1.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "launch list $?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_tc -s 40 -c 2 -o gpurun_out/prof_decode_r1 $CMD > gpurun_out/ncu_dec.log 2>&1; echo "ncu dec $?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:score_tc -s 2 -c 1 -o gpurun_out/prof_score_r1 $CMD > gpurun_out/ncu_score.log 2>&1; echo "ncu score $?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:score_tc -s 2 -c 2 -o gpurun_out/prof_score_r1 $CMD > gpurun_out/ncu_score.log 2>&1; echo "ncu score $?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:select -s 1 -c 1 -o gpurun_out/prof_select_r1 $CMD > gpurun_out/ncu_sel.log 2>&1; echo "ncu sel $?"
