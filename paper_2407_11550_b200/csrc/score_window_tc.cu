@@ -129,18 +129,27 @@ __device__ __forceinline__ void pool_inplace(float (&v)[NV]) {
     }
 }
 
-// pass-2 epilogue of one 32-output column group CG (outputs [32 CG, min(32 CG + 32, STEP)))
-template <int PAD, int CG>
-__device__ __forceinline__ void pass2_group(uint32_t taddr, int lane, int r, int key_col0, int n_o, float sl,
-                                            float lw2, uint8_t* a2tile, uint64_t* acc_empty_bar,
-                                            uint64_t* e_empty_bar, uint32_t e_parity, uint64_t* e_full_bar) {
+// pass-2 epilogue of one 32-output column group cg (outputs [32 cg, min(32 cg + 32, STEP))):
+// the column group is a runtime value so all 16 epilogue warps share one code path.  Always
+// 32 outputs are formed; the last group's surplus outputs (beyond the tile step) are zeros.
+template <int PAD>
+__device__ __forceinline__ void pass2_group_rt(int cg, uint32_t taddr, int lane, int r, int key_col0, int n_o,
+                                               float sl, float lw2, uint8_t* a2tile, uint64_t* acc_empty_bar,
+                                               uint64_t* e_empty_bar, uint32_t e_parity, uint64_t* e_full_bar) {
     constexpr int STEP = kTile - 2 * PAD;
-    constexpr int O0 = 32 * CG;                               // first output == first loaded column
-    constexpr int NOUT = (STEP - O0) < 32 ? (STEP - O0) : 32; // outputs of this group
-    constexpr int NV = (CG < 3 && PAD > 0) ? 40 : 32;         // loaded columns incl. the halo
+    constexpr int NV = PAD > 0 ? 40 : 32;  // loaded columns incl. the halo
+    const int O0 = 32 * cg;
+    const int NOUT = (STEP - O0) < 32 ? (STEP - O0) : 32;
     float v[NV];
     tmem_ld_x32<0>(taddr + O0, v);
-    if constexpr (NV > 32) tmem_ld_x8<32>(taddr + O0 + 32, v);
+    if constexpr (NV > 32) {
+        if (cg < 3) {
+            tmem_ld_x8<32>(taddr + O0 + 32, v);
+        } else {
+#pragma unroll
+            for (int jj = 32; jj < NV; ++jj) v[jj] = -INFINITY;
+        }
+    }
     tmem_ld_wait();
     tc_fence_before();
     __syncwarp();
@@ -152,25 +161,22 @@ __device__ __forceinline__ void pass2_group(uint32_t taddr, int lane, int r, int
         for (int jj = 0; jj < NV; ++jj)
             if (k0 + jj < 0 || k0 + jj >= n_o) v[jj] = -INFINITY;
     }
-    pool_inplace<PAD, NV, NOUT>(v);
+    pool_inplace<PAD, NV, 32>(v);
 #pragma unroll
-    for (int o = 0; o < NOUT; ++o) v[o] = fmaf(v[o], sl, -lw2);
-    exp2_mixed<NV, kPass2Poly>(v, NOUT);  // of every 8, kPass2Poly on the FMA pipe, the rest on MUFU
-    // E^T tile (fp16, MN-major SW128): window row r = K index, output o = M index
+    for (int o = 0; o < 32; ++o) v[o] = fmaf(v[o], sl, -lw2);
+    exp2_mixed<NV, kPass2Poly>(v, 32);
     mbar_wait(e_empty_bar, e_parity);
-    uint8_t* rowbase = a2tile + (r >> 3) * 2048 + (CG >> 1) * 1024 + (r & 7) * 128;
+    uint8_t* rowbase = a2tile + (r >> 3) * 2048 + (cg >> 1) * 1024 + (r & 7) * 128;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         uint32_t w[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int o0 = c * 8 + 2 * u, o1 = o0 + 1;
-            const float e0 = o0 < NOUT ? v[o0 < NOUT ? o0 : 0] : 0.f;
-            const float e1 = o1 < NOUT ? v[o1 < NOUT ? o1 : 0] : 0.f;
-            const __half2 h2 = __floats2half2_rn(e0, e1);
+            const __half2 h2 = __floats2half2_rn(o0 < NOUT ? v[o0] : 0.f, o1 < NOUT ? v[o1] : 0.f);
             w[u] = *reinterpret_cast<const uint32_t*>(&h2);
         }
-        const int chunk = 4 * (CG & 1) + c;
+        const int chunk = 4 * (cg & 1) + c;
         *reinterpret_cast<uint4*>(rowbase + ((chunk ^ (r & 7)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
     }
     fence_async_smem();
@@ -444,16 +450,8 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                     const uint32_t eb = j & 1, eph = (j >> 1) & 1;
                     const int key_col0 = t * prm.step - prm.pad;
                     const float lw = active ? lw2 : INFINITY;
-                    switch (cg) {
-                        case 0: pass2_group<PAD, 0>(taddr, lane, r, key_col0, prm.n_o, sl, lw, S.a2[eb], &S.acc_empty[ab],
-                                                    &S.e_empty[eb], eph ^ 1, &S.e_full[eb]); break;
-                        case 1: pass2_group<PAD, 1>(taddr, lane, r, key_col0, prm.n_o, sl, lw, S.a2[eb], &S.acc_empty[ab],
-                                                    &S.e_empty[eb], eph ^ 1, &S.e_full[eb]); break;
-                        case 2: pass2_group<PAD, 2>(taddr, lane, r, key_col0, prm.n_o, sl, lw, S.a2[eb], &S.acc_empty[ab],
-                                                    &S.e_empty[eb], eph ^ 1, &S.e_full[eb]); break;
-                        default: pass2_group<PAD, 3>(taddr, lane, r, key_col0, prm.n_o, sl, lw, S.a2[eb], &S.acc_empty[ab],
-                                                     &S.e_empty[eb], eph ^ 1, &S.e_full[eb]); break;
-                    }
+                    pass2_group_rt<PAD>(cg, taddr, lane, r, key_col0, prm.n_o, sl, lw, S.a2[eb], &S.acc_empty[ab],
+                                        &S.e_empty[eb], eph ^ 1, &S.e_full[eb]);
                     // one column group (rotating, so the extra work is spread evenly over the
                     // epilogue warps) reads back the scores of tile j-2
                     if (j > 1 && cg == int((j - 2) & 3)) readout(j - 2, prev2_pg, prev2_t);
