@@ -135,7 +135,8 @@ __device__ __forceinline__ void pool_inplace(float (&v)[NV]) {
 template <int PAD>
 __device__ __forceinline__ void pass2_group_rt(int cg, uint32_t taddr, int lane, int r, int key_col0, int n_o,
                                                float sl, float lw2, uint8_t* a2tile, uint64_t* acc_empty_bar,
-                                               uint64_t* e_empty_bar, uint32_t e_parity, uint64_t* e_full_bar) {
+                                               uint64_t* e_empty_bar, uint32_t e_parity, uint64_t* e_full_bar,
+                                               int dbg_flags) {
     constexpr int STEP = kTile - 2 * PAD;
     constexpr int NV = PAD > 0 ? 40 : 32;  // loaded columns incl. the halo
     const int O0 = 32 * cg;
@@ -164,7 +165,7 @@ __device__ __forceinline__ void pass2_group_rt(int cg, uint32_t taddr, int lane,
     pool_inplace<PAD, NV, 32>(v);
 #pragma unroll
     for (int o = 0; o < 32; ++o) v[o] = fmaf(v[o], sl, -lw2);
-    exp2_mixed<NV, kPass2Poly>(v, 32);
+    if (!(dbg_flags & 1024)) exp2_mixed<NV, kPass2Poly>(v, 32);
     mbar_wait(e_empty_bar, e_parity);
     uint8_t* rowbase = a2tile + (r >> 3) * 2048 + (cg >> 1) * 1024 + (r & 7) * 128;
 #pragma unroll
@@ -451,7 +452,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                     const int key_col0 = t * prm.step - prm.pad;
                     const float lw = active ? lw2 : INFINITY;
                     pass2_group_rt<PAD>(cg, taddr, lane, r, key_col0, prm.n_o, sl, lw, S.a2[eb], &S.acc_empty[ab],
-                                        &S.e_empty[eb], eph ^ 1, &S.e_full[eb]);
+                                        &S.e_empty[eb], eph ^ 1, &S.e_full[eb], prm.debug);
                     // one column group (rotating, so the extra work is spread evenly over the
                     // epilogue warps) reads back the scores of tile j-2
                     if (j > 1 && cg == int((j - 2) & 3)) readout(j - 2, prev2_pg, prev2_t);
