@@ -1,7 +1,9 @@
+# Round-end evidence run (one gpurun call, no profiler): GPU tests, smoke, the bench line
+# (with the CPU baseline), the reference arm and the per-stage timings.  Profiles: gpu_ncu.sh.
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -3 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?"; tail -2 gpurun_out/smoke.log
 timeout 1200 python bench.py > gpurun_out/bench_full.log 2>&1; echo "bench exit $?"; tail -1 gpurun_out/bench_full.log | cut -c1-300
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo "ref exit $?"; tail -1 gpurun_out/bench_ref.log | cut -c1-200
-timeout 300 python scripts/kbench.py --layers 32 > gpurun_out/kbench32.log 2>&1; tail -1 gpurun_out/kbench32.log
+timeout 300 python scripts/kbench.py --layers 32 > gpurun_out/kbench32.log 2>&1; tail -3 gpurun_out/kbench32.log

@@ -38,7 +38,11 @@ __global__ void k(long long* out, int nblk, int nslots, float scale_log2) {
     if (MODE == 3 || MODE == 6) {
         // K as the A operand (rows = keys): lane reads row gid and gid+8, 4 chunks each
         uint32_t ka[2][4];
-        for (int i = 0; i < 4; ++i) { ka[0][i] = box_off(gid, i * 4 + tig); ka[1][i] = box_off(gid + 8, i * 4 + tig); }
+        const int rho = (gid & 4) | ((gid & 1) << 1) | ((gid >> 1) & 1);  // quarter-warp rows {r, r+2}
+        for (int i = 0; i < 4; ++i) {
+            const int rr = MODE == 6 ? rho : gid;
+            ka[0][i] = box_off(rr, i * 4 + tig); ka[1][i] = box_off(rr + 8, i * 4 + tig);
+        }
         uint32_t qb[8][2];
         for (int st = 0; st < 8; ++st) { qb[st][0] = 0x3c003c00u + lane; qb[st][1] = 0x3c003c00u + st; }
         const int tsrc = ((gid & 3) >> 1) | ((gid & 1) << 1);  // lane (quad) publishing head gid&3
@@ -107,6 +111,68 @@ __global__ void k(long long* out, int nblk, int nslots, float scale_log2) {
             __syncwarp();
         }
         l_run = lh[0] + lh[1];
+    } else
+    if (MODE == 8) {
+        for (int j = 0; j < nblk; j += 2) {
+            uint4 kv[2][2][4], vv[2][4][2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t ks = slot0 + uint32_t(((j + u) % nslots) * 2 * kBoxBytes);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) { kv[u][0][i] = lds128(ks + koff[0][i]); kv[u][1][i] = lds128(ks + koff[1][i]); }
+#pragma unroll
+                for (int jv = 0; jv < 4; ++jv) { vv[u][jv][0] = lds128(ks + voff[jv][0]); vv[u][jv][1] = lds128(ks + voff[jv][1]); }
+            }
+            float x[2][4];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                float s0a[4] = {}, s1a[4] = {}, s0b[4] = {}, s1b[4] = {};
+#pragma unroll
+                for (int st = 0; st < 4; ++st) {
+                    const uint4 w0a = kv[u][0][st >> 1], w1a = kv[u][1][st >> 1], w0b = kv[u][0][2 + (st >> 1)], w1b = kv[u][1][2 + (st >> 1)];
+                    mma16816(s0a, qa0[st], 0u, qa2[st], 0u, (st & 1) ? w0a.z : w0a.x, (st & 1) ? w0a.w : w0a.y);
+                    mma16816(s1a, qa0[st], 0u, qa2[st], 0u, (st & 1) ? w1a.z : w1a.x, (st & 1) ? w1a.w : w1a.y);
+                    mma16816(s0b, qa0[4 + st], 0u, qa2[4 + st], 0u, (st & 1) ? w0b.z : w0b.x, (st & 1) ? w0b.w : w0b.y);
+                    mma16816(s1b, qa0[4 + st], 0u, qa2[4 + st], 0u, (st & 1) ? w1b.z : w1b.x, (st & 1) ? w1b.w : w1b.y);
+                }
+                x[u][0] = s0a[0] + s0b[0]; x[u][1] = s0a[1] + s0b[1]; x[u][2] = s1a[0] + s1b[0]; x[u][3] = s1a[1] + s1b[1];
+            }
+            float bm = fmaxf(fmaxf(fmaxf(x[0][0], x[0][1]), fmaxf(x[0][2], x[0][3])), fmaxf(fmaxf(x[1][0], x[1][1]), fmaxf(x[1][2], x[1][3])));
+            bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
+            bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
+            const float m_cand = fmaxf(m_run, bm * scale_log2);
+            const bool bump = m_cand > m_run + 8.f;
+            const float m_new = bump ? m_cand : m_run;
+            const float corr = bump ? ex2f(m_run - m_new) : 1.f;
+            const bool rescale = bump && m_run != -INFINITY;
+            float pp[2][4];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) pp[u][e] = ex2f(fmaf(x[u][e], scale_log2, -m_new));
+            l_run = l_run * corr + ((pp[0][0] + pp[0][1]) + (pp[0][2] + pp[0][3])) + ((pp[1][0] + pp[1][1]) + (pp[1][2] + pp[1][3]));
+            m_run = m_new;
+            if (__any_sync(0xffffffffu, rescale)) {
+                const float ca = __shfl_sync(0xffffffffu, corr, 8 * tig), cb = __shfl_sync(0xffffffffu, corr, 8 * tig + 4);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) { acc[i][0] *= ca; acc[i][1] *= cb; acc[i][2] *= ca; acc[i][3] *= cb; }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t b0 = pack_bf16(pp[u][0], pp[u][1]), b1 = pack_bf16(pp[u][2], pp[u][3]);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int h = i >> 2, wd = i & 3;
+                    const uint32_t* r0w = reinterpret_cast<const uint32_t*>(&vv[u][0][h]);
+                    const uint32_t* r1w = reinterpret_cast<const uint32_t*>(&vv[u][1][h]);
+                    const uint32_t* r8w = reinterpret_cast<const uint32_t*>(&vv[u][2][h]);
+                    const uint32_t* r9w = reinterpret_cast<const uint32_t*>(&vv[u][3][h]);
+                    mma16816(acc[i], __byte_perm(r0w[wd], r1w[wd], 0x5410), __byte_perm(r0w[wd], r1w[wd], 0x7632),
+                             __byte_perm(r8w[wd], r9w[wd], 0x5410), __byte_perm(r8w[wd], r9w[wd], 0x7632), b0, b1);
+                }
+            }
+            __syncwarp();
+        }
     } else
     for (int j = 0; j < nblk; ++j) {
         const int s = j % nslots;
@@ -191,17 +257,17 @@ __global__ void k(long long* out, int nblk, int nslots, float scale_log2) {
 int main() {
     long long* d; cudaMalloc(&d, 64 * 64 * sizeof(long long));
     const int nslots = 3, nblk = 64;
-    for (int mode : {0, 3, 6, 7}) {
+    for (int mode : {0, 7, 8}) {
         for (int W : {1, 2, 4, 8, 16}) {
             const size_t smem = size_t(W) * nslots * 2 * kBoxBytes + 1024;
-            auto kern = mode == 0 ? k<0> : mode == 3 ? k<3> : mode == 6 ? k<6> : k<7>;
+            auto kern = mode == 0 ? k<0> : mode == 7 ? k<7> : k<8>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (smem > 227 * 1024) continue;
             kern<<<1, 32 * W, smem>>>(d, nblk, nslots, 0.127f);
             kern<<<1, 32 * W, smem>>>(d, nblk, nslots, 0.127f);
             long long h[64]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
             long long mx = 0; for (int w = 0; w < W; ++w) mx = h[w] > mx ? h[w] : mx;
-            printf("mode %d (%s) W=%2d: %6.1f cycles/block/warp  (smem %.0f B/clk)\n", mode, mode == 0 ? "full" : mode == 1 ? "S+LDS" : mode == 2 ? "LDS" : mode == 3 ? "S^T full" : mode == 6 ? "S^T vote-max" : "vote-max", W,
+            printf("mode %d (%s) W=%2d: %6.1f cycles/block/warp  (smem %.0f B/clk)\n", mode, mode == 0 ? "full" : mode == 1 ? "S+LDS" : mode == 2 ? "LDS" : mode == 3 ? "S^T full" : mode == 7 ? "vote-max" : "pairs", W,
                    double(mx) / nblk, double(W) * nblk * 8192 / double(mx));
         }
     }
