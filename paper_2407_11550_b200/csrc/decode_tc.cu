@@ -136,7 +136,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
                  __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ seg_start,
                  int32_t* __restrict__ seqlens, const __nv_bfloat16* __restrict__ k_new,
                  const __nv_bfloat16* __restrict__ v_new, __nv_bfloat16* __restrict__ out, int H, int G,
-                 float scale_log2, int nslots, unsigned long long* __restrict__ dbg, int xflags) {
+                 float scale_log2, int nslots, unsigned long long* __restrict__ dbg) {
     constexpr int d = 128;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment by offsetting the __shared__ array itself (keeps the shared window,
@@ -254,7 +254,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         wstamp(j, 0);
         const int blk = (w_lo + j) * kBlk;
         const uint32_t ks = slot0 + uint32_t(s * 2 * kBoxBytes), vs = ks + kBoxBytes;
-        if (!(xflags & 1)) mbar_wait(&bars[s], sphase);
+        mbar_wait(&bars[s], sphase);
         wstamp(j, 1);
         if (blk + kBlk > L_old) {
             // the block holding the end of the segment: the appended row (produced upstream)
@@ -282,7 +282,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     if (nb > 0) fetch(0);
     // zdep is always 0 but depends on the fetched fragments, which pins the assembly below
     // after fetch(0) (otherwise the compiler hoists it, and with it the wait for Q)
-    const uint32_t zdep = (kv[0][0].x == 0x7fc00001u && xflags == -12345) ? 1u : 0u;
+    const uint32_t zdep = (kv[0][0].x == 0x7fc00001u && nslots == -12345) ? 1u : 0u;
     uint32_t qa0[8], qa2[8];
 #pragma unroll
     for (int st = 0; st < 8; ++st) {
@@ -512,15 +512,6 @@ static int decode_slots() {
     return n;
 }
 
-// (experiments) ADAKV_DECODE_XFLAGS: 1 = do not wait for the TMA data (timing only)
-static int decode_xflags() {
-    static int v = [] {
-        const char* e = std::getenv("ADAKV_DECODE_XFLAGS");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
 // Function attributes are per device: set them once for every device this process uses.
 static adakv_status prepare_kernel() {
     static std::mutex mu;
@@ -631,7 +622,7 @@ adakv_status launch_decode_tc(int64_t P, int64_t H, int64_t G, int32_t scale, co
     ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel_for(cs), tk, tv, static_cast<const __nv_bfloat16*>(q),
                                       static_cast<__nv_bfloat16*>(kc), static_cast<__nv_bfloat16*>(vc), ss, sl,
                                       static_cast<const __nv_bfloat16*>(kn), static_cast<const __nv_bfloat16*>(vn),
-                                      static_cast<__nv_bfloat16*>(out), int(H), int(G), sc, nslots, dbg_buf(), decode_xflags()));
+                                      static_cast<__nv_bfloat16*>(out), int(H), int(G), sc, nslots, dbg_buf()));
     return ADAKV_OK;
 }
 
