@@ -263,26 +263,30 @@ def run_ours(args, cfg):
                                   C.c_void_p(dg.out[0].data_ptr()), C.c_void_p(dg.ws.data_ptr()), dg.ws.numel(), st))
     torch.cuda.synchronize()
 
-    def decode_launches():
+    def decode_launches(dq_, dk_, dv_):
         stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         for s in range(S):
             for l in range(L):
                 seg = l * B * G
                 A._lib.check(lib.adakv_decode(
-                    2, B, H, G, d, 1, C.c_void_p(dq[s, l].data_ptr()), C.c_void_p(cache.k.data_ptr()),
+                    2, B, H, G, d, 1, C.c_void_p(dq_[s, l].data_ptr()), C.c_void_p(cache.k.data_ptr()),
                     C.c_void_p(cache.v.data_ptr()), cache.k.shape[0], C.c_void_p(cache.seg_start.data_ptr() + 4 * seg),
-                    C.c_void_p(cache.seqlens.data_ptr() + 4 * seg), max_rows, C.c_void_p(dk[s, l].data_ptr()),
-                    C.c_void_p(dv[s, l].data_ptr()), C.c_void_p(dg.out[l].data_ptr()), C.c_void_p(dg.ws.data_ptr()),
+                    C.c_void_p(cache.seqlens.data_ptr() + 4 * seg), max_rows, C.c_void_p(dk_[s, l].data_ptr()),
+                    C.c_void_p(dv_[s, l].data_ptr()), C.c_void_p(dg.out[l].data_ptr()), C.c_void_p(dg.ws.data_ptr()),
                     dg.ws.numel(), stream))
 
-    graph = torch.cuda.CUDAGraph()
-    cs = torch.cuda.Stream(device=dev)
-    cs.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(cs):
-        with torch.cuda.graph(graph, stream=cs):
-            decode_launches()
-    torch.cuda.current_stream().wait_stream(cs)
-    torch.cuda.synchronize()
+    def capture(dq_, dk_, dv_):
+        g_ = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream(device=dev)
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(g_, stream=cs):
+                decode_launches(dq_, dk_, dv_)
+        torch.cuda.current_stream().wait_stream(cs)
+        torch.cuda.synchronize()
+        return g_
+
+    graph = capture(dq, dk, dv)
 
     comp_ws = None
 
@@ -345,35 +349,58 @@ def run_ours(args, cfg):
         ms = float(t.item())
     value = ws * bytes_step / (ms * 1e-3) / 1e9
 
-    # ---- e2e through the public API with host buffers: H2D of the step's inputs from pinned
-    # memory, compress + decode, D2H of the step's result (final-step attention outputs + budgets)
+    # ---- e2e through the public API with host buffers: every step (one request) copies its
+    # inputs -- the prompt's window Q and K/V for every layer plus the decode-time q / k_new /
+    # v_new -- from pinned host memory, compresses, decodes, and reads back its result (final
+    # decode-step attention outputs + budgets).  Requests are double-buffered: the next
+    # request's inputs stream in on a copy stream while the current one compresses and
+    # decodes (two device input sets, one decode graph per set); the timed region spans the
+    # first copy to the last read-back, so every step's transfers are inside it.
     qh, kh, vh = q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory()
     dqh, dkh, dvh = dq.cpu().pin_memory(), dk.cpu().pin_memory(), dv.cpu().pin_memory()
     out_h = torch.empty(dg.out.shape, dtype=dg.out.dtype).pin_memory()
     bud_h = torch.empty(cache.budgets.shape, dtype=torch.int32).pin_memory()
     h2d = sum(x.numel() * x.element_size() for x in (qh, kh, vh, dqh, dkh, dvh))
     d2h = out_h.numel() * out_h.element_size() + bud_h.numel() * 4
+    sets = [(q, k, v, dq, dk, dv), tuple(torch.empty_like(x) for x in (q, k, v, dq, dk, dv))]
+    graphs = [graph, capture(*sets[1][3:])]
+    copy_st = torch.cuda.Stream(device=dev)
+    comp_st = torch.cuda.current_stream()
+    copied = [torch.cuda.Event(), torch.cuda.Event()]
+    done = [torch.cuda.Event(), torch.cuda.Event()]
 
-    def e2e_step():
-        q.copy_(qh, non_blocking=True)
-        k.copy_(kh, non_blocking=True)
-        v.copy_(vh, non_blocking=True)
-        dq.copy_(dqh, non_blocking=True)
-        dk.copy_(dkh, non_blocking=True)
-        dv.copy_(dvh, non_blocking=True)
-        step()
-        out_h.copy_(dg.out, non_blocking=True)
-        bud_h.copy_(cache.budgets, non_blocking=True)
+    def h2d_into(i):
+        with torch.cuda.stream(copy_st):
+            copy_st.wait_event(done[i])  # the set's previous request has finished with it
+            for dst, src in zip(sets[i], (qh, kh, vh, dqh, dkh, dvh)):
+                dst.copy_(src, non_blocking=True)
+            copied[i].record(copy_st)
 
-    e2e_step()
+    def e2e_run(nreq):
+        for i in range(2):
+            done[i].record(comp_st)
+        h2d_into(0)
+        for r in range(nreq):
+            i = r & 1
+            if r + 1 < nreq:
+                h2d_into(i ^ 1)
+            comp_st.wait_event(copied[i])
+            qi, ki, vi = sets[i][:3]
+            PL.compress_model(qi, ki, vi, LB, reserve=reserve, out=cache)
+            graphs[i].replay()
+            done[i].record(comp_st)
+            out_h.copy_(dg.out, non_blocking=True)
+            bud_h.copy_(cache.budgets, non_blocking=True)
+
+    e2e_run(2)
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
-    t0.record()
-    ne2e = max(1, min(args.steps, 3))
-    for _ in range(ne2e):
-        e2e_step()
-    t1.record()
+    ne2e = max(2, min(args.steps, 5))
+    t0.record(comp_st)
+    copy_st.wait_event(t0)
+    e2e_run(ne2e)
+    t1.record(comp_st)
     torch.cuda.synchronize()
     e2e_ms = t0.elapsed_time(t1) / ne2e
     if ws > 1:
@@ -381,6 +408,7 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_val = ws * bytes_step / (e2e_ms * 1e-3) / 1e9
+    del sets, graphs
 
     # ---- derived numbers + roofline of the dominant kernel
     peak, src = measured_peaks()
@@ -424,7 +452,8 @@ def run_ours(args, cfg):
         "decode_us_per_layer_step": round(dec_launch_us, 3),
         "roofline": roof, "clocks": clk.result, "gpu_launches": launches,
         "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms, 3)},
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms, 3), "requests": ne2e,
+                "overlap": "next request's H2D on a copy stream during the current compress + decode"},
         "peak_source": src,
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
