@@ -248,13 +248,13 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     };
     int s = 0;
     uint32_t sphase = 0;  // slot and mbarrier phase of block j (no division in the loop)
-    uint4 kv[2][4], vv[4][2];
-    // block j's fragments: wait for its slot, patch the segment end, load K and V fragments
-    auto fetch = [&](int j) {
+    auto slot_addr = [&](int sl) { return slot0 + uint32_t(sl * 2 * kBoxBytes); };
+    // block j's K fragments: wait for its slot (sl, ph), patch the segment end, load K
+    auto fetch_k = [&](int j, int sl, uint32_t ph, uint4 (&kv)[2][4]) {
         wstamp(j, 0);
         const int blk = (w_lo + j) * kBlk;
-        const uint32_t ks = slot0 + uint32_t(s * 2 * kBoxBytes), vs = ks + kBoxBytes;
-        mbar_wait(&bars[s], sphase);
+        const uint32_t ks = slot_addr(sl), vs = ks + kBoxBytes;
+        mbar_wait(&bars[sl], ph);
         wstamp(j, 1);
         if (blk + kBlk > L_old) {
             // the block holding the end of the segment: the appended row (produced upstream)
@@ -271,18 +271,22 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             kv[0][i] = lds128(ks + koff[0][i]);
             kv[1][i] = lds128(ks + koff[1][i]);
         }
+    };
+    auto load_v = [&](int sl, uint4 (&vv)[4][2]) {
+        const uint32_t ks = slot_addr(sl);
 #pragma unroll
         for (int jv = 0; jv < 4; ++jv) {
             vv[jv][0] = lds128(ks + voff[jv][0]);
             vv[jv][1] = lds128(ks + voff[jv][1]);
         }
     };
-    // the first block's wait and fragment loads go before the Q fragments are assembled
-    // (register moves that wait for the Q loads), so they overlap the Q latency
-    if (nb > 0) fetch(0);
+    // the first block's wait and K loads go before the Q fragments are assembled (register
+    // moves that wait for the Q loads), so they overlap the Q latency
+    uint4 kva[2][4], kvb[2][4];
+    if (nb > 0) fetch_k(0, 0, 0u, kva);
     // zdep is always 0 but depends on the fetched fragments, which pins the assembly below
-    // after fetch(0) (otherwise the compiler hoists it, and with it the wait for Q)
-    const uint32_t zdep = (kv[0][0].x == 0x7fc00001u && nslots == -12345) ? 1u : 0u;
+    // after fetch_k(0) (otherwise the compiler hoists it, and with it the wait for Q)
+    const uint32_t zdep = (kva[0][0].x == 0x7fc00001u && nslots == -12345) ? 1u : 0u;
     uint32_t qa0[8], qa2[8];
 #pragma unroll
     for (int st = 0; st < 8; ++st) {
@@ -290,10 +294,10 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         qa0[st] = ((st & 1) ? w.z : w.x) ^ zdep;
         qa2[st] = ((st & 1) ? w.w : w.y) ^ zdep;
     }
-    for (int j = 0; j < nb; ++j) {
-        if (j > 0) fetch(j);
+    // S = Q K^T of block j: two key tiles x two halves of d -> four independent 4-deep MMA
+    // chains; keys past the segment end are masked
+    auto scores = [&](int j, const uint4 (&kv)[2][4], float (&x)[4]) {
         const int blk = (w_lo + j) * kBlk;
-        // S = Q K^T: two key tiles x two halves of d -> four independent 4-deep MMA chains
         float s0a[4] = {0.f, 0.f, 0.f, 0.f}, s1a[4] = {0.f, 0.f, 0.f, 0.f};
         float s0b[4] = {0.f, 0.f, 0.f, 0.f}, s1b[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -305,29 +309,36 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             mma16816(s0b, qa0[4 + st], 0u, qa2[4 + st], 0u, (st & 1) ? w0b.z : w0b.x, (st & 1) ? w0b.w : w0b.y);
             mma16816(s1b, qa0[4 + st], 0u, qa2[4 + st], 0u, (st & 1) ? w1b.z : w1b.x, (st & 1) ? w1b.w : w1b.y);
         }
-        float x0 = s0a[0] + s0b[0], x1 = s0a[1] + s0b[1], x2 = s1a[0] + s1b[0], x3 = s1a[1] + s1b[1];
-        wstamp(j, 2);
-        if (blk + kBlk > L) {  // keys past the segment end
-            if (blk + rv0 >= L) x0 = -INFINITY;
-            if (blk + rv1 >= L) x1 = -INFINITY;
-            if (blk + 8 + rv0 >= L) x2 = -INFINITY;
-            if (blk + 8 + rv1 >= L) x3 = -INFINITY;
+        x[0] = s0a[0] + s0b[0];
+        x[1] = s0a[1] + s0b[1];
+        x[2] = s1a[0] + s1b[0];
+        x[3] = s1a[1] + s1b[1];
+        if (blk + kBlk > L) {
+            if (blk + rv0 >= L) x[0] = -INFINITY;
+            if (blk + rv1 >= L) x[1] = -INFINITY;
+            if (blk + 8 + rv0 >= L) x[2] = -INFINITY;
+            if (blk + 8 + rv1 >= L) x[3] = -INFINITY;
         }
-        float bm = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3));
+    };
+    // online softmax over the keys in x[0..NX) (one or two blocks): lazy running max -- it
+    // moves only when the keys exceed it by more than 8 (log2 units), so probabilities stay
+    // <= 2^8 and the accumulator is rescaled rarely; the first block needs no rescale
+    auto softmax = [&](float* x, int nx) {
+        float bm = -INFINITY;
+        for (int i = 0; i < nx; ++i) bm = fmaxf(bm, x[i]);
         bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
         bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
-        // lazy running max: the reference moves only when a block exceeds it by more than 8
-        // (log2 units), so probabilities stay <= 2^8 and the accumulator is rescaled rarely;
-        // the first block needs no rescale (acc and l are still zero)
         const float m_cand = fmaxf(m_run, bm * scale_log2);
         const bool bump = m_cand > m_run + 8.f;
         const float m_new = bump ? m_cand : m_run;
         const float corr = bump ? ex2f(m_run - m_new) : 1.f;
         const bool rescale = bump && m_run != -INFINITY;
-        float p0 = ex2f(fmaf(x0, scale_log2, -m_new)), p1 = ex2f(fmaf(x1, scale_log2, -m_new));
-        float p2 = ex2f(fmaf(x2, scale_log2, -m_new)), p3 = ex2f(fmaf(x3, scale_log2, -m_new));
-        if (!head_ok) p0 = p1 = p2 = p3 = 0.f;
-        l_run = l_run * corr + ((p0 + p1) + (p2 + p3));
+        float lsum = 0.f;
+        for (int i = 0; i < nx; ++i) {
+            x[i] = head_ok ? ex2f(fmaf(x[i], scale_log2, -m_new)) : 0.f;
+            lsum += x[i];
+        }
+        l_run = l_run * corr + lsum;
         m_run = m_new;
         if (__any_sync(0xffffffffu, head_ok && rescale)) {
             const float ca = __shfl_sync(0xffffffffu, corr, 8 * tig);
@@ -340,7 +351,10 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
                 acc[i][3] *= cb;
             }
         }
-        const uint32_t b0 = pack_bf16(p0, p1), b1 = pack_bf16(p2, p3);
+    };
+    // O^T += V^T P^T for one block (p = its four probabilities)
+    auto pv = [&](const uint4 (&vv)[4][2], const float* pr) {
+        const uint32_t b0 = pack_bf16(pr[0], pr[1]), b1 = pack_bf16(pr[2], pr[3]);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int h = i >> 2, wd = i & 3;
@@ -351,13 +365,53 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             mma16816(acc[i], __byte_perm(r0w[wd], r1w[wd], 0x5410), __byte_perm(r0w[wd], r1w[wd], 0x7632),
                      __byte_perm(r8w[wd], r9w[wd], 0x5410), __byte_perm(r8w[wd], r9w[wd], 0x7632), b0, b1);
         }
-        __syncwarp();  // every lane's reads of slot s have been consumed
-        if (lane == 0 && j + nslots < nb) issue(j + nslots);
-        wstamp(j, 3);
-        if (++s == nslots) {
-            s = 0;
-            sphase ^= 1u;
+    };
+    auto advance = [&](int& sl, uint32_t& ph) {
+        if (++sl == nslots) {
+            sl = 0;
+            ph ^= 1u;
         }
+    };
+    // Blocks are taken two at a time when the warp has two left: both blocks' S chains, one
+    // softmax over 32 keys, then both PVs -- the two blocks' latency chains overlap.
+    int j = 0;
+    while (j < nb) {
+        if (j + 1 < nb) {
+            int s1 = s;
+            uint32_t ph1 = sphase;
+            advance(s1, ph1);
+            fetch_k(j + 1, s1, ph1, kvb);
+            float x[8];
+            scores(j, kva, *reinterpret_cast<float(*)[4]>(&x[0]));
+            scores(j + 1, kvb, *reinterpret_cast<float(*)[4]>(&x[4]));
+            wstamp(j, 2);
+            softmax(x, 8);
+            uint4 vv[4][2];
+            load_v(s, vv);
+            pv(vv, &x[0]);
+            load_v(s1, vv);
+            pv(vv, &x[4]);
+            __syncwarp();  // every lane's reads of both slots have been consumed
+            if (lane == 0 && j + nslots < nb) issue(j + nslots);
+            if (lane == 0 && j + 1 + nslots < nb) issue(j + 1 + nslots);
+            wstamp(j, 3);
+            s = s1;
+            sphase = ph1;
+            advance(s, sphase);
+            j += 2;
+        } else {
+            float x[4];
+            scores(j, kva, x);
+            softmax(x, 4);
+            uint4 vv[4][2];
+            load_v(s, vv);
+            pv(vv, x);
+            __syncwarp();
+            if (lane == 0 && j + nslots < nb) issue(j + nslots);
+            advance(s, sphase);
+            j += 1;
+        }
+        if (j < nb) fetch_k(j, s, sphase, kva);
     }
     stamp(3);
     if (dbg && lane == 0 && warp < 8) {  // (debug) every warp's loop end + its block count

@@ -1,2 +1,4 @@
-timeout 600 python bench.py --no-cpu-baseline --steps 5 --warmup 3 > gpurun_out/bq.log 2>&1; echo "exit $?"; tail -3 gpurun_out/bq.log | cut -c1-200
-tail -1 gpurun_out/bq.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["decode_us_per_layer_step"], d["compress_ms_per_layer"], d["e2e"])'
+timeout 600 python -m pytest tests/ -m gpu -x -q -p no:cacheprovider -k "decode" 2>&1 | tail -2
+for i in 1 2; do NOSTAMP=1 timeout 300 python scripts/dec_ts4.py 2>&1 | tail -1; done
+timeout 300 python scripts/dec_ts4.py 2>&1 | grep -v Warn | grep "clk\|warp loop"
+timeout 300 python bench.py --no-cpu-baseline --steps 3 --warmup 3 2>/dev/null | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["decode_us_per_layer_step"], d["compress_ms_per_layer"])'
