@@ -440,43 +440,50 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     }
     __syncthreads();
     stamp(4);
-    // ---- (2) CTA merge of the W warp partials: thread -> (column c, head quad hq); the result
-    // (relative to the CTA max) goes to the rank owning column c
+    // ---- (2) CTA merge of the W warp partials: thread -> (column c, head quad hq).  The W x 4
+    // per-(warp, head) scales are the same for every column, so each lane of a merging warp
+    // computes one of them (lane = 4 w + head; W = 8 covers the warp) and the column loop
+    // takes them with shuffles instead of recomputing 32 exponentials per thread.
+    static_assert(W == 8, "one scale per lane: 8 warps x 4 heads");
     {
         const int nq = (gs + 3) >> 2;
         for (int t = threadIdx.x; t < 128 * nq; t += 32 * W) {
-            const int c = t / nq, hq = t % nq;
-            float M[4], Lh[4];
+            const int hq = t >> 7, c = t & 127;  // head quad is uniform over a warp
+            const int fw = lane >> 2, fh = 4 * hq + (lane & 3);
+            const float mw = S.s_ml[fw][fh][0];
+            float M = mw;
+            M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 4));
+            M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 8));
+            M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 16));
+            const float f = mw == -INFINITY ? 0.f : ex2f(mw - M);
+            float lf = S.s_ml[fw][fh][1] * f;
+            lf += __shfl_xor_sync(0xffffffffu, lf, 4);
+            lf += __shfl_xor_sync(0xffffffffu, lf, 8);
+            lf += __shfl_xor_sync(0xffffffffu, lf, 16);  // lanes 0..3: the head's scaled sum
             float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int jh = 0; jh < 4; ++jh) {
-                M[jh] = -INFINITY;
-#pragma unroll
-                for (int w = 0; w < W; ++w) M[jh] = fmaxf(M[jh], S.s_ml[w][4 * hq + jh][0]);
-                Lh[jh] = 0.f;
-            }
-#pragma unroll
             for (int w = 0; w < W; ++w) {
-                float f[4];
-#pragma unroll
-                for (int jh = 0; jh < 4; ++jh) {
-                    const float m = S.s_ml[w][4 * hq + jh][0];
-                    f[jh] = m == -INFINITY ? 0.f : ex2f(m - M[jh]);
-                    Lh[jh] += S.s_ml[w][4 * hq + jh][1] * f[jh];
-                }
+                const float f0 = __shfl_sync(0xffffffffu, f, 4 * w + 0), f1 = __shfl_sync(0xffffffffu, f, 4 * w + 1);
+                const float f2 = __shfl_sync(0xffffffffu, f, 4 * w + 2), f3 = __shfl_sync(0xffffffffu, f, 4 * w + 3);
                 const float4 o = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(ring_of(w)) + so_idx(c, 4 * hq));
-                O.x += o.x * f[0];
-                O.y += o.y * f[1];
-                O.z += o.z * f[2];
-                O.w += o.w * f[3];
+                O.x += o.x * f0;
+                O.y += o.y * f1;
+                O.z += o.z * f2;
+                O.w += o.w * f3;
+            }
+            float Mq[4], Lq[4];
+#pragma unroll
+            for (int jh = 0; jh < 4; ++jh) {
+                Mq[jh] = __shfl_sync(0xffffffffu, M, jh);
+                Lq[jh] = __shfl_sync(0xffffffffu, lf, jh);
             }
             const int owner = ((c + 1) * CS - 1) / d, cl = c - (d * owner) / CS;
             // straight into the owner's receive chunk for this rank (DSMEM st.async)
             const uint32_t dst = smem_u32(S.recv + rank * chunk), bar = mapa(smem_u32(&S.rbar), owner);
             st_async_v4(mapa(dst + 4u * uint32_t(16 + cl * 8 + 4 * hq), owner), O, bar);
             if (cl == 0) {
-                st_async_v4(mapa(dst + 4u * uint32_t(8 * hq), owner), make_float4(M[0], Lh[0], M[1], Lh[1]), bar);
-                st_async_v4(mapa(dst + 4u * uint32_t(8 * hq + 4), owner), make_float4(M[2], Lh[2], M[3], Lh[3]), bar);
+                st_async_v4(mapa(dst + 4u * uint32_t(8 * hq), owner), make_float4(Mq[0], Lq[0], Mq[1], Lq[1]), bar);
+                st_async_v4(mapa(dst + 4u * uint32_t(8 * hq + 4), owner), make_float4(Mq[2], Lq[2], Mq[3], Lq[3]), bar);
             }
         }
     }
