@@ -11,10 +11,17 @@
 // so under programmatic dependent launch a layer's cache streams in while the previous
 // layer's decode is still finishing.
 //
-// Per warp, keys are consumed in blocks of 16:
+// Per warp, keys are consumed in blocks of 16, two blocks per step when two are left (their
+// S chains overlap; one softmax covers the 32 keys):
 //   S  = Q K^T      two m16n8k16 n8 tiles x 8 k-steps; rows = the g heads (padded to 16);
-//   P  = exp2(S*c - m)  online softmax (block max over the 4 lanes of a row);
+//   P  = exp2(S*c - m)  online softmax (block max over the 4 lanes of a row; the running
+//                   max moves only when a step exceeds it by more than 2^8);
 //   O^T += V^T P^T  eight m16n8k16 m-tiles over d.
+// The per-block cost is the mma.sync issue/latency chain (scripts/micro/dec_block.cu), so
+// the first block's wait and K loads are placed before the Q fragments are assembled (the
+// Q load's latency overlaps them).  Combine: warp partials merge in shared memory (each
+// (warp, head) scale computed once per merging warp and shared by shuffles), then each CTA
+// pushes its columns' slice to the owning rank with DSMEM st.async.
 // The dot products are invariant to a consistent permutation of d, so Q's and K's
 // d-columns are permuted such that each lane's B-fragment words are exactly the 16-byte
 // chunks it reads; V's d (the MMA M dimension) is permuted likewise and un-permuted when O
