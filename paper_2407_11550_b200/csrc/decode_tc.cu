@@ -209,6 +209,13 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         for (int j = 0; j < (nb < nslots ? nb : nslots); ++j) issue(j);
     }
     __syncwarp();
+    // warm L2 with this lane's Q row while the previous layer finishes: an L2 prefetch is
+    // safe before the dependency wait (it fills no L1 line, and L2 is the point of coherence
+    // for the producer's writes), and the loads after the wait then hit L2
+    {
+        const char* qrow = reinterpret_cast<const char*>(q + (int64_t(p) * H + g * gs + (head_ok ? gid : 0)) * d);
+        if (warp == 0 && tig < 2) asm volatile("prefetch.global.L2 [%0];" ::"l"(qrow + 128 * tig) : "memory");
+    }
     stamp(1);
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
