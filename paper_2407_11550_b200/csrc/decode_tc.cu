@@ -278,6 +278,15 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
                 const bool isnew = append && blk + rr == L_old;
                 sts128(dst + box_off(rr, lane & 15), isnew ? new_chunk : make_uint4(0, 0, 0, 0));
             }
+            // K5 append, by the warp holding the new row's block: no other CTA's boxes cover
+            // it, this CTA's own box has landed, and every CTA of the cluster read seqlens
+            // before the cluster barrier, so the row and the length are written here, from
+            // the registers already holding the row, instead of at the end of the kernel
+            if (append && L_old >= blk) {
+                reinterpret_cast<uint4*>((lane < 16 ? k_cache : v_cache) + (int64_t(base) + L_old) * d)[lane & 15] =
+                    new_chunk;
+                if (lane == 0) seqlens[pg] = L;
+            }
             __syncwarp();
         }
 #pragma unroll
@@ -520,16 +529,6 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             Os += ch[16 + cl * 8 + h] * f;
         }
         out[(int64_t(p) * H + g * gs + h) * d + col_lo + cl] = __float2bfloat16_rn(Os / Ls);
-    }
-    // every rank read seqlens and its rows before sending its chunk, and rank 0 has them all
-    if (rank == 0 && append) {
-        if (threadIdx.x < 32) {  // K5 append: the new row lands after the window rows
-            const __nv_bfloat16* kn = k_new + int64_t(pg) * d;
-            const __nv_bfloat16* vn = v_new + int64_t(pg) * d;
-            reinterpret_cast<uint2*>(k_cache + (int64_t(base) + L_old) * d)[threadIdx.x] = reinterpret_cast<const uint2*>(kn)[threadIdx.x];
-            reinterpret_cast<uint2*>(v_cache + (int64_t(base) + L_old) * d)[threadIdx.x] = reinterpret_cast<const uint2*>(vn)[threadIdx.x];
-        }
-        if (threadIdx.x == 0) seqlens[pg] = L;
     }
     stamp(7);
 }
