@@ -66,6 +66,7 @@ __host__ __device__ constexpr int chunk_floats(int cs) { return 16 + ((128 + cs 
 // Shared memory: the split-K combine buffers, then the per-warp TMA rings.
 struct DecSmem {
     float s_ml[kMaxWarps][8][2];                    // warp partials: (m, l) per head
+    alignas(16) float s_f[kMaxWarps][32];           // CTA merge: each merging warp's 32 scales
     alignas(16) float recv[kMaxCS * 16 + 1024 + kMaxCS * 8];   // one chunk from every rank
     uint64_t bar[kMaxWarps][kMaxSlots];
     uint64_t rbar;                                  // receive barrier (bulk-copy complete_tx)
@@ -466,7 +467,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     // ---- (2) CTA merge of the W warp partials: thread -> (column c, head quad hq).  The W x 4
     // per-(warp, head) scales are the same for every column, so each lane of a merging warp
     // computes one of them (lane = 4 w + head; W = 8 covers the warp) and the column loop
-    // takes them with shuffles instead of recomputing 32 exponentials per thread.
+    // reads them back as broadcast float4s instead of recomputing 32 exponentials per thread.
     static_assert(W == 8, "one scale per lane: 8 warps x 4 heads");
     {
         const int nq = (gs + 3) >> 2;
@@ -483,17 +484,19 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             lf += __shfl_xor_sync(0xffffffffu, lf, 4);
             lf += __shfl_xor_sync(0xffffffffu, lf, 8);
             lf += __shfl_xor_sync(0xffffffffu, lf, 16);  // lanes 0..3: the head's scaled sum
+            S.s_f[warp][lane] = f;
+            __syncwarp();
             float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
             for (int w = 0; w < W; ++w) {
-                const float f0 = __shfl_sync(0xffffffffu, f, 4 * w + 0), f1 = __shfl_sync(0xffffffffu, f, 4 * w + 1);
-                const float f2 = __shfl_sync(0xffffffffu, f, 4 * w + 2), f3 = __shfl_sync(0xffffffffu, f, 4 * w + 3);
+                const float4 fw4 = *reinterpret_cast<const float4*>(&S.s_f[warp][4 * w]);  // broadcast
                 const float4 o = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(ring_of(w)) + so_idx(c, 4 * hq));
-                O.x += o.x * f0;
-                O.y += o.y * f1;
-                O.z += o.z * f2;
-                O.w += o.w * f3;
+                O.x += o.x * fw4.x;
+                O.y += o.y * fw4.y;
+                O.z += o.z * fw4.z;
+                O.w += o.w * fw4.w;
             }
+            __syncwarp();  // s_f[warp] is rewritten by the next column round
             float Mq[4], Lq[4];
 #pragma unroll
             for (int jh = 0; jh < 4; ++jh) {
