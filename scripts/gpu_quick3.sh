@@ -1,6 +1,2 @@
-python - <<'PY'
-import paper_2407_11550_b200 as A
-L = A.lib()
-print("cluster", L.adakv_debug_decode_cluster(1, 8))
-PY
-timeout 300 python bench.py --no-cpu-baseline --steps 3 --warmup 3 2>/dev/null | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["decode_us_per_layer_step"])'
+for dbg in 0 1 0 1; do ADAKV_TC_DEBUG=$dbg timeout 120 python scripts/tc_time.py 8 2>&1 | tail -1; done
+timeout 800 python -m pytest tests/ -m gpu -x -q -p no:cacheprovider 2>&1 | tail -1
