@@ -488,3 +488,42 @@ def test_decode_umma_variant_vs_oracle(dev, oracle_mod):
                 assert err <= 2e-2 and err <= 1e-2 * max(np.abs(ref).max(), 1e-3) + 4e-3, (step, p, err)
     finally:
         L.adakv_debug_decode_umma(prev)
+
+
+@pytest.mark.parametrize("H,G", [(2, 2), (6, 2), (10, 2), (12, 2), (14, 2), (16, 2)])
+def test_decode_bf16_group_sizes_append(dev, oracle_mod, H, G):
+    """The tensor-core decode at every group size g = H/G in 1..8 (head quads, padded heads,
+    the CTA merge's (warp, head) lanes), two steps with appends: outputs within the bf16
+    tolerance of the fp64 oracle, the appended rows and lengths exact."""
+    from paper_2407_11550_b200.ops import CompressedCache
+    O = oracle_mod
+    rng = np.random.default_rng(H * 10 + G)
+    d, steps = 128, 2
+    lens = rng.integers(150, 700, size=G).astype(np.int32)
+    caps = lens + steps + 2
+    starts = np.concatenate([[0], np.cumsum(caps)[:-1]]).astype(np.int32)
+    rows = int(caps.sum())
+    kp = torch.as_tensor(rng.normal(size=(rows, d)) * 0.5).to(torch.bfloat16).to(dev)
+    vp = torch.as_tensor(rng.normal(size=(rows, d))).to(torch.bfloat16).to(dev)
+    cache = CompressedCache(k=kp, v=vp, seg_start=torch.as_tensor(starts, device=dev),
+                            seqlens=torch.as_tensor(lens, device=dev), budgets=torch.as_tensor(lens, device=dev),
+                            P=1, H=H, G=G, m=0, d=d, reserve=steps + 2, layer_budget=int(lens.sum()))
+    segs = [[x.double().cpu().numpy() for x in cache.segment(0, g)] for g in range(G)]
+    for step in range(steps):
+        qd = torch.as_tensor(rng.normal(size=(1, H, d))).to(torch.bfloat16).to(dev)
+        kn = torch.as_tensor(rng.normal(size=(1, G, d))).to(torch.bfloat16).to(dev)
+        vn = torch.as_tensor(rng.normal(size=(1, G, d))).to(torch.bfloat16).to(dev)
+        o = A.decode(qd, cache, kn, vn, max_rows=int(caps.max()))
+        for g in range(G):
+            segs[g][0] = np.vstack([segs[g][0], kn[0, g].double().cpu().numpy()])
+            segs[g][1] = np.vstack([segs[g][1], vn[0, g].double().cpu().numpy()])
+        off = np.concatenate([[0], np.cumsum([s[0].shape[0] for s in segs])])
+        ref = O.decode_attention(qd[0].double().cpu().numpy(), np.vstack([s[0] for s in segs]),
+                                 np.vstack([s[1] for s in segs]), off)
+        err = np.abs(o[0].double().cpu().numpy() - ref).max()
+        assert err <= 2e-2 and err <= 1e-2 * max(np.abs(ref).max(), 1e-3) + 4e-3, (step, err)
+        assert cache.seqlens.cpu().tolist() == [s[0].shape[0] for s in segs]
+        for g in range(G):
+            kr, vr = cache.segment(0, g)
+            assert np.array_equal(kr.double().cpu().numpy(), segs[g][0])
+            assert np.array_equal(vr.double().cpu().numpy(), segs[g][1])
