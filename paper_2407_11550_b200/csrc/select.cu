@@ -494,9 +494,19 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     for (int s = tid; s < S; s += kSelThreads) {
         int64_t eqb = 0, kept = 0;
         const int64_t need = seg_mode[s] == MODE_THRESH ? seg_need[s] : 0;
-        for (unsigned r = 0; r < rank; ++r) {
-            const uint32_t* rc = cluster.map_shared_rank(&ccnt[0][0], r);
-            const int64_t g = rc[s * 2 + 0], q = rc[s * 2 + 1];
+        uint32_t rg[8], rq[8];  // every lower rank's counts, all remote loads in flight at once
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            rg[r] = rq[r] = 0u;
+            if (unsigned(r) < rank) {
+                const uint32_t* rc = cluster.map_shared_rank(&ccnt[0][0], r);
+                rg[r] = rc[s * 2 + 0];
+                rq[r] = rc[s * 2 + 1];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int64_t g = rg[r], q = rq[r];
             const int64_t t = need - eqb;
             kept += g + (t <= 0 ? 0 : (t < q ? t : q));
             eqb += q;
@@ -510,24 +520,35 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         for (int s = 0; s < S; ++s) t += seg_kept_before[s];
         cta_kept_before = t;
     }
-    for (int s = tid; s < S; s += kSelThreads) {
-        int64_t eqb = seg_eqb[s];
+    // per segment, one warp: lane w takes warp w's counts; the T-equal counts of the warps
+    // before it are an exclusive prefix sum over the lanes (kWarps == 32)
+    static_assert(kWarps == 32, "lane per warp");
+    for (int s = warp; s < S; s += kWarps) {
         const int64_t need = seg_mode[s] == MODE_THRESH ? seg_need[s] : 0;
-        for (int w = 0; w < kWarps; ++w) {
-            const int64_t g = wcnt[(w * S + s) * 2 + 0], q = wcnt[(w * S + s) * 2 + 1];
-            const int64_t t = need - eqb;
-            wkept[w * S + s] = g + (t <= 0 ? 0 : (t < q ? t : q));
-            weqb[w * S + s] = eqb;
-            eqb += q;
+        const int64_t g = wcnt[(lane * S + s) * 2 + 0], q = wcnt[(lane * S + s) * 2 + 1];
+        int64_t inc = q;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
         }
+        const int64_t eqb = seg_eqb[s] + inc - q;
+        const int64_t t = need - eqb;
+        wkept[lane * S + s] = g + (t <= 0 ? 0 : (t < q ? t : q));
+        weqb[lane * S + s] = eqb;
     }
     __syncthreads();
-    if (tid == 0) {
-        int64_t run = cta_kept_before;
-        for (int w = 0; w < kWarps; ++w) {
-            wkept_before[w] = run;
-            for (int s = 0; s < S; ++s) run += wkept[w * S + s];
+    // kept elements before each warp: lane w's total over segments, exclusive prefix over lanes
+    if (warp == 0) {
+        int64_t tot = 0;
+        for (int s = 0; s < S; ++s) tot += wkept[lane * S + s];
+        int64_t inc = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
         }
+        wkept_before[lane] = cta_kept_before + inc - tot;
     }
     __syncthreads();
     {
@@ -535,17 +556,21 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         uint8_t* keep_out = prm.keep ? prm.keep + p * N : nullptr;
         int32_t* kp = prm.kept_pos ? prm.kept_pos + p * prm.kept_stride : nullptr;
         for (int s = 0; s < S; ++s) {
-            const int64_t a = max(wlo, prm.off[s]), b = min(whi, prm.off[s + 1]);
+            // everything the element loop reads is loaded once here: its byte stores may alias
+            // any generic address, which would otherwise force a reload per element
+            const int64_t off_s = prm.off[s], off_e = prm.off[s + 1];
+            const int64_t a = max(wlo, off_s), b = min(whi, off_e);
             if (a >= b) continue;
             const int mode = seg_mode[s];
             const KT T = seg_T[s];
             const int64_t need = seg_need[s];
-            const int64_t n = prm.off[s + 1] - prm.off[s];
+            const int64_t n = off_e - off_s;
+            const int64_t sink = seg_sink[s], recent_lo = n - seg_recent[s];
             int64_t run_eq = weqb[warp * S + s];
             for (int64_t base = a; base < b; base += 32) {
                 const int64_t e = base + lane;
                 const bool valid = e < b;
-                const int64_t pos = e - prm.off[s];
+                const int64_t pos = e - off_s;
                 bool keep = false;
                 if (mode == MODE_THRESH) {
                     KT u = 0;
@@ -558,7 +583,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                 } else if (mode == MODE_ALL) {
                     keep = valid;
                 } else if (mode == MODE_STREAM) {
-                    keep = valid && (pos < seg_sink[s] || pos >= n - seg_recent[s]);
+                    keep = valid && (pos < sink || pos >= recent_lo);
                 }
                 const unsigned bk = __ballot_sync(0xffffffffu, keep);
                 if (keep && kp) kp[run_kept + __popc(bk & lt)] = int32_t(pos);
