@@ -146,10 +146,19 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         have_hist0 = 0;
         g_k = prm.totals ? prm.totals[p] : prm.total;
     }
+    // segment tables read by every pass: offsets, the ranks holding each segment's elements
+    // (the only ranks whose histograms the DSMEM sum reads) and this CTA's segment range
+    __shared__ int64_t s_off[kMaxSeg + 1];
+    __shared__ unsigned char seg_r0[kMaxSeg], seg_r1[kMaxSeg];
+    __shared__ int c_s0, c_s1;
+    for (int s = tid; s <= S; s += kSelThreads) s_off[s] = prm.off[s];
     for (int s = tid; s < S; s += kSelThreads) {
         seg_gt[s] = 0;
         b_caps[s] = uint64_t(prm.off[s + 1] - prm.off[s]);
+        seg_r0[s] = (unsigned char)((prm.off[s] * CS) / N);
+        seg_r1[s] = (unsigned char)(((prm.off[s + 1] > 0 ? prm.off[s + 1] - 1 : 0) * CS) / N);
     }
+
     // Every pass below re-reads this CTA's slice of keys: read the scores from global memory
     // once, in coalesced order, and keep the order-preserving keys in shared memory.
     const bool cached = prm.cache_keys != 0;
@@ -158,6 +167,19 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     auto key_at = [&](int64_t e) -> KT { return cached ? kc[e - lo] : KeyOf<F>::get(sc[e]); };
     __syncthreads();
     stamp();
+    if (tid == 0) {
+        // the segments whose DSMEM sum reads this rank's histograms (the same rank ranges as
+        // the sum uses, so an empty segment at a slice boundary is covered too); published
+        // by the barriers of the min/max step below
+        int s0 = S, s1 = -1;
+        for (int s = 0; s < S; ++s)
+            if (seg_r0[s] <= rank && rank <= seg_r1[s]) {
+                s0 = s < s0 ? s : s0;
+                s1 = s;
+            }
+        c_s0 = s0;
+        c_s1 = s1;
+    }
 
     // Bits shared by every key of the problem are skipped: the radix digits start at the
     // highest bit where the problem's min and max keys differ.  (Scores concentrate in a
@@ -231,8 +253,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         const KT mask = hi_mask(pass);
         uint32_t* hb = hist + buf * S * 256;
         uint32_t* my = wh + warp * 256;  // this warp's private histogram (no inter-warp atomics)
-        for (int s = 0; s < S; ++s) {
-            const int64_t a = max(lo, prm.off[s]), b = min(hi, prm.off[s + 1]);
+        // only segments overlapping this CTA's slice: no other rank's DSMEM sum reads the rest
+        for (int s = c_s0; s <= c_s1; ++s) {
+            const int64_t a = max(lo, s_off[s]), b = min(hi, s_off[s + 1]);
             if (!seg_active[s] || a >= b) {
                 for (int i = tid; i < 256; i += kSelThreads) hb[s * 256 + i] = 0;
                 continue;
@@ -278,14 +301,24 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         cluster.sync();
         // sum the CS histograms through DSMEM: all remote loads issued before any is used
         // (segment s has elements only in ranks [r0, r1]: the others' histograms are zero)
-        for (int i = tid; i < S * 256; i += kSelThreads) {
-            const int sg = i >> 8;
-            const unsigned r0 = unsigned((prm.off[sg] * CS) / N);
-            const unsigned r1 = unsigned(((prm.off[sg + 1] > 0 ? prm.off[sg + 1] - 1 : 0) * CS) / N);
-            uint32_t v[8];
+        for (int i0 = tid; i0 < S * 256; i0 += 2 * kSelThreads) {
+            uint32_t v[2][8];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) v[r] = (unsigned(r) + r0 <= r1) ? cluster.map_shared_rank(hb, r0 + r)[i] : 0u;
-            agg[i] = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+            for (int u = 0; u < 2; ++u) {
+                const int i = i0 + u * kSelThreads;
+                const int sg = i >> 8;
+                const bool in = i < S * 256;
+                const unsigned r0 = in ? seg_r0[sg] : 1u, r1 = in ? seg_r1[sg] : 0u;
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                    v[u][r] = (unsigned(r) + r0 <= r1) ? cluster.map_shared_rank(hb, r0 + r)[i] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int i = i0 + u * kSelThreads;
+                if (i < S * 256)
+                    agg[i] = ((v[u][0] + v[u][1]) + (v[u][2] + v[u][3])) + ((v[u][4] + v[u][5]) + (v[u][6] + v[u][7]));
+            }
         }
         __syncthreads();
         buf ^= 1;
