@@ -267,14 +267,18 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
             if (cached) {
                 // 16-byte vector reads of the cached keys: V consecutive keys per thread
                 constexpr int V = 16 / int(sizeof(KT));
-                const int64_t a0 = a - lo, b0 = b - lo;
-                for (int64_t base = (a0 / V) * V + int64_t(tid) * V; base < b0; base += int64_t(kSelThreads) * V) {
+                // (slice-local indices fit 32 bits; only the vectors straddling the segment
+                // ends need per-key range checks)
+                const int a0 = int(a - lo), b0 = int(b - lo);
+                for (int base = (a0 / V) * V + tid * V; base < b0; base += kSelThreads * V) {
                     const uint4 raw = *reinterpret_cast<const uint4*>(kc + base);
                     const KT* kk = reinterpret_cast<const KT*>(&raw);
+                    const bool full = base >= a0 && base + V <= b0;
 #pragma unroll
                     for (int i = 0; i < V; ++i) {
                         const KT u = kk[i];
-                        if (base + i >= a0 && base + i < b0 && (u & mask) == pre)
+                        const bool in = full || (base + i >= a0 && base + i < b0);
+                        if (in && (u & mask) == pre)
                             atomicAdd(&my[int((u >> shift) & 0xFF)], 1u);  // warp-private histogram
                     }
                 }
