@@ -604,14 +604,17 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
             const int64_t n = off_e - off_s;
             const int64_t sink = seg_sink[s], recent_lo = n - seg_recent[s];
             int64_t run_eq = weqb[warp * S + s];
-            for (int64_t base = a; base < b; base += 32) {
-                const int64_t e = base + lane;
-                const bool valid = e < b;
-                const int64_t pos = e - off_s;
+            // 32-bit element offsets from the warp's range start (ranges fit 32 bits)
+            const int len = int(b - a);
+            const int pos0 = int(a - off_s);
+            for (int o = 0; o < len; o += 32) {
+                const int j = o + lane;
+                const bool valid = j < len;
+                const int pos = pos0 + j;
                 bool keep = false;
                 if (mode == MODE_THRESH) {
                     KT u = 0;
-                    if (valid) u = key_at(e);
+                    if (valid) u = key_at(a + j);
                     const bool is_eq = valid && u == T;
                     const unsigned beq = __ballot_sync(0xffffffffu, is_eq);
                     const int64_t eqr = run_eq + __popc(beq & lt);
@@ -624,7 +627,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                 }
                 const unsigned bk = __ballot_sync(0xffffffffu, keep);
                 if (keep && kp) kp[run_kept + __popc(bk & lt)] = int32_t(pos);
-                if (valid && keep_out) keep_out[e] = keep ? 1 : 0;
+                if (valid && keep_out) keep_out[a + j] = keep ? 1 : 0;
                 run_kept += __popc(bk);
             }
         }
