@@ -1,1 +1,2 @@
-for v in 1 0 1 0; do if [ $v = 1 ]; then export E2E_ONE_STREAM=1; else unset E2E_ONE_STREAM; fi; echo "one_stream=$v $(timeout 600 python bench.py --no-cpu-baseline --steps 5 --warmup 3 2>/dev/null | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["e2e"]["value"], d["e2e"]["ms_per_step"])')"; done
+# bench line's e2e leg only (device + host-link timing of the double-buffered requests)
+timeout 600 python bench.py --no-cpu-baseline --steps 5 --warmup 3 2>/dev/null | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["e2e"])'
