@@ -79,9 +79,16 @@ gather_kernel(const V* __restrict__ k, const V* __restrict__ v, int64_t G, int64
     const int64_t total = cum[G];
     const int64_t r0 = int64_t(blockIdx.x) * kRowsPerBlock;
     const int64_t r1 = min(r0 + int64_t(kRowsPerBlock), total);
-    const int64_t items = (r1 - r0) * vec_per_row;
-    for (int64_t it = threadIdx.x; it < items; it += kGatherThreads) {
-        const int64_t r = r0 + it / vec_per_row, c = it % vec_per_row;
+    const int nrow = int(r1 - r0), vpr = int(vec_per_row);
+    // vec_per_row is a power of two for every supported row size (d * esize / sizeof(V)):
+    // row and column of an item by shift and mask, in 32 bits (no 64-bit division per item)
+    const int vshift = __ffs(vpr) - 1;
+    const bool pow2 = (vpr & (vpr - 1)) == 0;
+    const int items = nrow * vpr;
+    for (int it = threadIdx.x; it < items; it += kGatherThreads) {
+        const int rr = pow2 ? (it >> vshift) : it / vpr;
+        const int c = pow2 ? (it & (vpr - 1)) : it % vpr;
+        const int64_t r = r0 + rr;
         int64_t g = 0;
         while (cum[g + 1] <= r) ++g;
         const int64_t rin = r - cum[g];
