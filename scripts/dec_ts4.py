@@ -17,11 +17,12 @@ if os.environ.get("NOPDL"):
     L.adakv_set_decode_overlap(0)
 dev = torch.device("cuda:0")
 Lyr, H, G, d, LB = int(os.environ.get("LAYERS", "32")), 32, 8, 128, 16384
+B = int(os.environ.get("BATCH", "1"))
 steps = int(os.environ.get("STEPS", "4"))
 reserve = steps + 8
 rng = np.random.default_rng(0)
 lens = []
-for l in range(Lyr):
+for l in range(Lyr * B):
     w = rng.lognormal(0, float(os.environ.get("SKEW", "0.05")), G)
     x = np.floor(w / w.sum() * LB).astype(np.int64)
     x[0] += LB - x.sum()
@@ -33,9 +34,9 @@ rows = int(caps.sum())
 kp = (torch.randn((rows, d), device=dev) * 0.5).to(torch.bfloat16)
 vp = torch.randn((rows, d), device=dev).to(torch.bfloat16)
 cache = CompressedCache(k=kp, v=vp, seg_start=torch.as_tensor(starts, device=dev), seqlens=torch.as_tensor(lens, device=dev),
-                        budgets=torch.as_tensor(lens, device=dev), P=Lyr, H=H, G=G, m=0, d=d, reserve=reserve,
+                        budgets=torch.as_tensor(lens, device=dev), P=Lyr * B, H=H, G=G, m=0, d=d, reserve=reserve,
                         layer_budget=LB)
-dg = PL.DecodeGraph(cache, Lyr, 1, LB + reserve, use_graph=False)
+dg = PL.DecodeGraph(cache, Lyr, B, LB + reserve, use_graph=False)
 dg.q.normal_()
 nl = steps * Lyr
 dbg = torch.zeros((nl, 256, 32), dtype=torch.int64, device=dev)
@@ -48,9 +49,9 @@ with torch.cuda.stream(st):
         for s in range(steps):
             for l in range(Lyr):
                 L.adakv_debug_set_decode_timestamps(C.c_void_p(dbg[s * Lyr + l].data_ptr()) if stamp else None)
-                seg = l * G
+                seg = l * B * G
                 A._lib.check(L.adakv_decode(
-                    2, 1, H, G, d, 1, C.c_void_p(dg.q[l].data_ptr()), C.c_void_p(cache.k.data_ptr()),
+                    2, B, H, G, d, 1, C.c_void_p(dg.q[l].data_ptr()), C.c_void_p(cache.k.data_ptr()),
                     C.c_void_p(cache.v.data_ptr()), cache.k.shape[0], C.c_void_p(cache.seg_start.data_ptr() + 4 * seg),
                     C.c_void_p(cache.seqlens.data_ptr() + 4 * seg), LB + reserve, C.c_void_p(dg.k_new[l].data_ptr()),
                     C.c_void_p(dg.v_new[l].data_ptr()), C.c_void_p(dg.out[l].data_ptr()), C.c_void_p(dg.ws.data_ptr()),
@@ -66,7 +67,7 @@ e0.record()
 g.replay()
 e1.record()
 torch.cuda.synchronize()
-cs = L.adakv_debug_decode_cluster(1, G)
+cs = L.adakv_debug_decode_cluster(B, G)
 print(f"cluster {cs}; graph: {nl} launches, {e0.elapsed_time(e1) * 1e3 / nl:.2f} us/launch; segment rows {lens.min()}..{lens.max()}")
 if not stamp:
     sys.exit(0)

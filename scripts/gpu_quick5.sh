@@ -1,2 +1,1 @@
-timeout 800 python -m pytest tests/ -m gpu -x -q -p no:cacheprovider 2>&1 | tail -1
-for i in 1 2; do timeout 300 python scripts/kbench.py --layers 32 2>&1 | tail -3 | head -2 | cut -c1-200; done
+for b in 1 2 4 8; do echo "batch $b: $(BATCH=$b NOSTAMP=1 timeout 300 python scripts/dec_ts4.py 2>&1 | tail -1)"; done
