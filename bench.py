@@ -199,6 +199,14 @@ def run_reference(args, cfg):
         "e2e": {"value": round(gbs, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "peak_source": src,
     }
+    if scal:
+        pk = measured_peaks()[0]
+        line["decode_batch_scaling"] = {
+            "note": "supplementary, not the headline: one decode launch per layer carrying B requests, "
+                    "synthetic caches of this config's shape",
+            "batch": sorted(scal), "us_per_launch": [round(scal[b][0], 3) for b in sorted(scal)],
+            "gbs": [round(scal[b][1], 1) for b in sorted(scal)],
+            "frac": [round(scal[b][1] / pk, 4) for b in sorted(scal)]}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -212,6 +220,70 @@ def config_obj(cfg, args):
             "budget_per_head": cfg["budget"], "layer_budget": cfg["budget"] * cfg["G"], "policy": "ada_snapkv",
             "alpha": 0.2, "pool_kernel": 7, "decode_steps": cfg["decode_steps"], "parallelism": f"batch{args.gpus}",
             "l2": "inputs exceed L2 (2.1 GB prompt K per request), no flush"}
+
+
+def decode_batch_scaling(dev, H, G, d, L, budget_rows, batches=(1, 8), steps=4, seed=5):
+    """Supplementary (not the headline): the same decode kernel at larger batches -- one launch
+    per layer carrying B requests' segments (~budget_rows rows each, +-11% spread like the
+    bench's adaptive budgets), `steps` decode steps x L layers in one CUDA graph with the PDL
+    chain, caches HBM-resident.  Returns {B: (us per launch, GB/s)}."""
+    import ctypes as C
+    import torch
+    import paper_2407_11550_b200 as A
+    from paper_2407_11550_b200 import pipeline as PL
+    from paper_2407_11550_b200.ops import CompressedCache
+    lib = A.lib()
+    rng = np.random.default_rng(seed)
+    res = {}
+    for B in batches:
+        P = L * B
+        w = rng.uniform(0.89, 1.11, size=(P, G))
+        lens = np.floor(w / w.sum(axis=1, keepdims=True) * budget_rows * G).astype(np.int32)
+        caps = lens + steps + 2
+        starts = np.concatenate([[0], np.cumsum(caps.ravel())[:-1]]).astype(np.int32)
+        rows = int(caps.sum())
+        kp = (torch.randn((rows, d), device=dev) * 0.5).to(torch.bfloat16)
+        vp = torch.randn((rows, d), device=dev).to(torch.bfloat16)
+        seq0 = torch.as_tensor(lens.ravel(), device=dev)
+        cache = CompressedCache(k=kp, v=vp, seg_start=torch.as_tensor(starts, device=dev), seqlens=seq0.clone(),
+                                budgets=seq0.clone(), P=P, H=H, G=G, m=0, d=d, reserve=steps + 2,
+                                layer_budget=int(budget_rows * G))
+        dg = PL.DecodeGraph(cache, L, B, int(caps.max()), use_graph=False)
+        dg.q.normal_()
+        dq = torch.randn((steps, L, B, H, d), device=dev).to(torch.bfloat16)
+        dk = torch.randn((steps, L, B, G, d), device=dev).to(torch.bfloat16)
+        st = torch.cuda.Stream(device=dev)
+        st.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(st):
+            with torch.cuda.graph(g, stream=st):
+                for s in range(steps):
+                    for l in range(L):
+                        seg = l * B * G
+                        A._lib.check(lib.adakv_decode(
+                            2, B, H, G, d, 1, C.c_void_p(dq[s, l].data_ptr()), C.c_void_p(kp.data_ptr()),
+                            C.c_void_p(vp.data_ptr()), rows, C.c_void_p(cache.seg_start.data_ptr() + 4 * seg),
+                            C.c_void_p(cache.seqlens.data_ptr() + 4 * seg), int(caps.max()),
+                            C.c_void_p(dk[s, l].data_ptr()), C.c_void_p(dk[s, l].data_ptr()),
+                            C.c_void_p(dg.out[l].data_ptr()), C.c_void_p(dg.ws.data_ptr()), dg.ws.numel(),
+                            C.c_void_p(st.cuda_stream)))
+        torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        g.replay()  # warm
+        cache.seqlens.copy_(seq0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / (steps * L)
+        attended = steps * int(lens.sum()) + P * G * steps * (steps + 1) // 2
+        nbytes = 2 * 2 * d * attended + steps * P * (2 * 2 * H * d + 2 * 2 * G * d)
+        res[B] = (us, nbytes / (steps * L) / (us * 1e-6) / 1e9)
+        del g, dg, cache, kp, vp, dq, dk
+        torch.cuda.empty_cache()
+    return res
 
 
 def run_ours(args, cfg):
@@ -410,6 +482,9 @@ def run_ours(args, cfg):
     e2e_val = ws * bytes_step / (e2e_ms * 1e-3) / 1e9
     del sets, graphs
 
+    # ---- supplementary: the decode kernel at batch 1 and 8 (same shapes, synthetic caches)
+    scal = decode_batch_scaling(dev, H, G, d, L, cfg["budget"]) if ws == 1 else {}
+
     # ---- derived numbers + roofline of the dominant kernel
     peak, src = measured_peaks()
     cm, dm, sm_ = float(np.median(comp_ms)), float(np.median(dec_ms)), float(np.median(sc_ms))
@@ -456,6 +531,14 @@ def run_ours(args, cfg):
                 "overlap": "next request's H2D on a copy stream during the current compress + decode"},
         "peak_source": src,
     }
+    if scal:
+        pk = measured_peaks()[0]
+        line["decode_batch_scaling"] = {
+            "note": "supplementary, not the headline: one decode launch per layer carrying B requests, "
+                    "synthetic caches of this config's shape",
+            "batch": sorted(scal), "us_per_launch": [round(scal[b][0], 3) for b in sorted(scal)],
+            "gbs": [round(scal[b][1], 1) for b in sorted(scal)],
+            "frac": [round(scal[b][1] / pk, 4) for b in sorted(scal)]}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         try:
