@@ -15,6 +15,11 @@ value = whole-step algorithmic GB/s (compress bytes + decode bytes, SURVEY.md §
         over all ranks / max-over-ranks device time; the compress and decode halves are
         reported separately (compress_ms_per_layer, decode_gbs) with their roofline fractions.
 
+e2e: the same metric through the public API with every request's inputs copied from pinned
+host memory and its result read back, requests double-buffered (the next one's H2D overlaps
+the current compress + decode).  decode_batch_scaling (supplementary): the decode kernel at
+batch 1 and 8 on synthetic caches of this shape.
+
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 Multi-GPU (torchrun): independent requests shard by batch, one per rank (weak scaling,
 no data-path collective).
@@ -264,7 +269,7 @@ def decode_batch_scaling(dev, H, G, d, L, budget_rows, batches=(1, 8), steps=4, 
                             2, B, H, G, d, 1, C.c_void_p(dq[s, l].data_ptr()), C.c_void_p(kp.data_ptr()),
                             C.c_void_p(vp.data_ptr()), rows, C.c_void_p(cache.seg_start.data_ptr() + 4 * seg),
                             C.c_void_p(cache.seqlens.data_ptr() + 4 * seg), int(caps.max()),
-                            C.c_void_p(dk[s, l].data_ptr()), C.c_void_p(dk[s, l].data_ptr()),
+                            C.c_void_p(dk[s, l].data_ptr()), C.c_void_p(dk[s, l].data_ptr()),  # k_new, v_new
                             C.c_void_p(dg.out[l].data_ptr()), C.c_void_p(dg.ws.data_ptr()), dg.ws.numel(),
                             C.c_void_p(st.cuda_stream)))
         torch.cuda.current_stream().wait_stream(st)
