@@ -531,7 +531,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             Ls += ch[2 * h + 1] * f;
             Os += ch[16 + cl * 8 + h] * f;
         }
-        out[(int64_t(p) * H + g * gs + h) * d + col_lo + cl] = __float2bfloat16_rn(Os / Ls);
+        out[(int64_t(p) * H + g * gs + h) * d + col_lo + cl] = __float2bfloat16_rn(__fdividef(Os, Ls));
     }
     stamp(7);
 }

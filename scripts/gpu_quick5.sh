@@ -1,2 +1,2 @@
-for cs in 5 6 7 8 9; do echo "B2 cs $cs: $(BATCH=2 ADAKV_DECODE_CS=$cs NOSTAMP=1 timeout 300 python scripts/dec_ts4.py 2>&1 | tail -1)"; done
-for cs in 3 4 5; do echo "B4 cs $cs: $(BATCH=4 ADAKV_DECODE_CS=$cs NOSTAMP=1 timeout 300 python scripts/dec_ts4.py 2>&1 | tail -1)"; done
+timeout 800 python -m pytest tests/ -m gpu -x -q -p no:cacheprovider -k "decode" 2>&1 | tail -1
+for i in 1 2; do timeout 300 python bench.py --no-cpu-baseline --steps 3 --warmup 3 2>/dev/null | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["decode_us_per_layer_step"])'; done
