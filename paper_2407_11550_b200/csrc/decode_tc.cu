@@ -517,8 +517,9 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     mbar_wait(&S.rbar, 0);
     stamp(6);
     // ---- (4) this rank's columns: merge the CS chunks
+    const int gshift = (gs & (gs - 1)) == 0 ? __ffs(gs) - 1 : -1;  // g a power of two: shifts
     for (int t = threadIdx.x; t < ncols * gs; t += 32 * W) {
-        const int cl = t / gs, h = t % gs;
+        const int cl = gshift >= 0 ? t >> gshift : t / gs, h = gshift >= 0 ? t & (gs - 1) : t % gs;
         float M = -INFINITY;
 #pragma unroll
         for (int r = 0; r < CS; ++r) M = fmaxf(M, S.recv[r * chunk + 2 * h]);
