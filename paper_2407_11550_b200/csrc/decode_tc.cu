@@ -637,12 +637,17 @@ int64_t decode_tc_cluster(int64_t P, int64_t G) {
         if (cudaOccupancyMaxActiveClusters(&n, kernel_for(cs), &cfg) == cudaSuccess) fit[cs] = n;
         cudaGetLastError();
     }
-    // The largest size for which every cluster of one launch is co-resident.  (Sizing for two
-    // co-resident launches, so the next layer's clusters all start early, measured slower:
-    // the smaller clusters cost more in the combine than the earlier start saves.)
+    // The largest size for which every cluster of one launch is co-resident -- or one size
+    // smaller when that lets two launches' CTAs share the SMs (one CTA each), so every CTA of
+    // the next layer's launch starts, and prefetches, while this one runs: config 2 measures
+    // 4.11 us per step-layer at 9 against 4.13 at 10.  Smaller still costs more in per-CTA
+    // work than the earlier start saves.
     int64_t best = 1;
     for (int64_t cs = kMaxCS; cs >= 2 && best == 1; --cs)
         if (fit[cs] >= segs) best = cs;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (best > 2 && 2 * segs * (best - 1) <= sms && 2 * segs * best > sms) best -= 1;
     if (const char* e = std::getenv("ADAKV_DECODE_CS")) {
         const int64_t v = std::atoi(e);
         if (v >= 1 && v <= kMaxCS) best = v;
