@@ -204,14 +204,6 @@ def run_reference(args, cfg):
         "e2e": {"value": round(gbs, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "peak_source": src,
     }
-    if scal:
-        pk = measured_peaks()[0]
-        line["decode_batch_scaling"] = {
-            "note": "supplementary, not the headline: one decode launch per layer carrying B requests, "
-                    "synthetic caches of this config's shape",
-            "batch": sorted(scal), "us_per_launch": [round(scal[b][0], 3) for b in sorted(scal)],
-            "gbs": [round(scal[b][1], 1) for b in sorted(scal)],
-            "frac": [round(scal[b][1] / pk, 4) for b in sorted(scal)]}
     print(json.dumps(line), flush=True)
     return 0
 
