@@ -217,6 +217,27 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         const char* qrow = reinterpret_cast<const char*>(q + (int64_t(p) * H + g * gs + (head_ok ? gid : 0)) * d);
         if (warp == 0 && tig < 2) asm volatile("prefetch.global.L2 [%0];" ::"l"(qrow + 128 * tig) : "memory");
     }
+    // register set-up that needs nothing produced upstream: done before the dependency wait
+    float m_run = -INFINITY, l_run = 0.f;
+    float acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+
+    const int rk0 = kperm(gid), rk1 = 8 + kperm(gid);                // K rows of this lane (tiles 0, 1)
+    const int rv0 = kperm(2 * tig), rv1 = kperm(2 * tig + 1);         // V rows of key slots 2t, 2t+1 (+8)
+    // loop-invariant fragment offsets within a slot (the per-block work is then base + offset)
+    uint32_t koff[2][4], voff[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        koff[0][i] = box_off(rk0, i * 4 + tig);
+        koff[1][i] = box_off(rk1, i * 4 + tig);
+    }
+#pragma unroll
+    for (int jv = 0; jv < 4; ++jv) {
+        const int r = (jv >> 1) * 8 + ((jv & 1) ? rv1 : rv0);
+        voff[jv][0] = kBoxBytes + box_off(r, gid);
+        voff[jv][1] = kBoxBytes + box_off(r, 8 + gid);
+    }
     stamp(1);
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -238,26 +259,6 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     uint4 new_chunk = make_uint4(0, 0, 0, 0);
     if (append && nb > 0 && (w_hi * kBlk > L_old))
         new_chunk = reinterpret_cast<const uint4*>((lane < 16 ? k_new : v_new) + int64_t(pg) * d)[lane & 15];
-    float m_run = -INFINITY, l_run = 0.f;
-    float acc[8][4];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-
-    const int rk0 = kperm(gid), rk1 = 8 + kperm(gid);                // K rows of this lane (tiles 0, 1)
-    const int rv0 = kperm(2 * tig), rv1 = kperm(2 * tig + 1);         // V rows of key slots 2t, 2t+1 (+8)
-    // loop-invariant fragment offsets within a slot (the per-block work is then base + offset)
-    uint32_t koff[2][4], voff[4][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        koff[0][i] = box_off(rk0, i * 4 + tig);
-        koff[1][i] = box_off(rk1, i * 4 + tig);
-    }
-#pragma unroll
-    for (int jv = 0; jv < 4; ++jv) {
-        const int r = (jv >> 1) * 8 + ((jv & 1) ? rv1 : rv0);
-        voff[jv][0] = kBoxBytes + box_off(r, gid);
-        voff[jv][1] = kBoxBytes + box_off(r, 8 + gid);
-    }
     auto wstamp = [&](int j, int k) {  // (debug) warp 1's first two blocks: cycles per phase
         if (dbg && warp == 1 && lane == 0 && j < 2) dbg[blockIdx.x * 32 + 8 + 4 * j + k] = clock64();
     };
