@@ -527,3 +527,40 @@ def test_decode_bf16_group_sizes_append(dev, oracle_mod, H, G):
             kr, vr = cache.segment(0, g)
             assert np.array_equal(kr.double().cpu().numpy(), segs[g][0])
             assert np.array_equal(vr.double().cpu().numpy(), segs[g][1])
+
+
+def test_decode_bf16_tiny_and_empty_segments_append(dev, oracle_mod):
+    """Segments of 0..40 rows (empty before the append, single partial blocks, most warps and
+    CTAs without blocks): three appended steps, outputs within tolerance, rows exact."""
+    from paper_2407_11550_b200.ops import CompressedCache
+    O = oracle_mod
+    rng = np.random.default_rng(11)
+    H, G, d, steps = 32, 8, 128, 3
+    lens = np.array([0, 1, 2, 15, 16, 17, 31, 40], dtype=np.int32)
+    caps = lens + steps + 1
+    starts = np.concatenate([[0], np.cumsum(caps)[:-1]]).astype(np.int32)
+    rows = int(caps.sum())
+    kp = torch.as_tensor(rng.normal(size=(rows, d)) * 0.5).to(torch.bfloat16).to(dev)
+    vp = torch.as_tensor(rng.normal(size=(rows, d))).to(torch.bfloat16).to(dev)
+    cache = CompressedCache(k=kp, v=vp, seg_start=torch.as_tensor(starts, device=dev),
+                            seqlens=torch.as_tensor(lens, device=dev), budgets=torch.as_tensor(lens, device=dev),
+                            P=1, H=H, G=G, m=0, d=d, reserve=steps + 1, layer_budget=int(lens.sum()))
+    segs = [[x.double().cpu().numpy() for x in cache.segment(0, g)] for g in range(G)]
+    for step in range(steps):
+        qd = torch.as_tensor(rng.normal(size=(1, H, d))).to(torch.bfloat16).to(dev)
+        kn = torch.as_tensor(rng.normal(size=(1, G, d))).to(torch.bfloat16).to(dev)
+        vn = torch.as_tensor(rng.normal(size=(1, G, d))).to(torch.bfloat16).to(dev)
+        o = A.decode(qd, cache, kn, vn, max_rows=int(caps.max()))
+        for g in range(G):
+            segs[g][0] = np.vstack([segs[g][0], kn[0, g].double().cpu().numpy()])
+            segs[g][1] = np.vstack([segs[g][1], vn[0, g].double().cpu().numpy()])
+        off = np.concatenate([[0], np.cumsum([s[0].shape[0] for s in segs])])
+        ref = O.decode_attention(qd[0].double().cpu().numpy(), np.vstack([s[0] for s in segs]),
+                                 np.vstack([s[1] for s in segs]), off)
+        err = np.abs(o[0].double().cpu().numpy() - ref).max()
+        assert err <= 2e-2 and err <= 1e-2 * max(np.abs(ref).max(), 1e-3) + 4e-3, (step, err)
+        assert cache.seqlens.cpu().tolist() == [s[0].shape[0] for s in segs]
+        for g in range(G):
+            kr, vr = cache.segment(0, g)
+            assert np.array_equal(kr.double().cpu().numpy(), segs[g][0])
+            assert np.array_equal(vr.double().cpu().numpy(), segs[g][1])
