@@ -107,6 +107,15 @@ __device__ __forceinline__ void exp2_mixed(float (&x)[N], int count) {
     }
 }
 
+// v[c] = v[c] * sl - m for c < N, two columns per packed FFMA2
+template <int N, int NV>
+__device__ __forceinline__ void scale_shift2(float (&v)[NV], float sl, float m) {
+    static_assert(N % 2 == 0 && N <= NV, "pairs");
+    const uint64_t s2 = pk(sl, sl), m2 = pk(-m, -m);
+#pragma unroll
+    for (int c = 0; c < N; c += 2) upk(fma2(pk(v[c], v[c + 1]), s2, m2), v[c], v[c + 1]);
+}
+
 // in-place max-pool of width 2*PAD+1: v[o] = max(v[o .. o + 2 PAD]) for o < NOUT
 template <int PAD, int NV, int NOUT>
 __device__ __forceinline__ void pool_inplace(float (&v)[NV]) {
@@ -163,8 +172,7 @@ __device__ __forceinline__ void pass2_group_rt(int cg, uint32_t taddr, int lane,
             if (k0 + jj < 0 || k0 + jj >= n_o) v[jj] = -INFINITY;
     }
     pool_inplace<PAD, NV, 32>(v);
-#pragma unroll
-    for (int o = 0; o < 32; ++o) v[o] = fmaf(v[o], sl, -lw2);
+    scale_shift2<32>(v, sl, lw2);
     if (!(dbg_flags & 1024)) exp2_mixed<NV, kPass2Poly>(v, 32);
     mbar_wait(e_empty_bar, e_parity);
     uint8_t* rowbase = a2tile + (r >> 3) * 2048 + (cg >> 1) * 1024 + (r & 7) * 128;
@@ -429,8 +437,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                     const float tmx = fmaxf(m2[0], m2[1]);
                     const float nm = fmaxf(run_m, tmx * sl);
                     if (nm != -INFINITY) {
-#pragma unroll
-                        for (int c = 0; c < 32; ++c) v[c] = fmaf(v[c], sl, -nm);
+                        scale_shift2<32>(v, sl, nm);
                         // 2 of every 8 exp2 on the FMA pipe (polynomial), 6 on MUFU: measured
                         // fastest split (debug 64: MUFU only)
                         if (prm.debug & 64) exp2_mixed<32, 0>(v, 32);
