@@ -418,32 +418,55 @@ def run_ours(args, cfg):
         ms = float(t.item())
     value = ws * bytes_step / (ms * 1e-3) / 1e9
 
-    # ---- e2e through the public API with host buffers: every step (one request) copies its
+    # ---- e2e through the public API with host buffers: every step (one request) takes its
     # inputs -- the prompt's window Q and K/V for every layer plus the decode-time q / k_new /
     # v_new -- from pinned host memory, compresses, decodes, and reads back its result (final
-    # decode-step attention outputs + budgets).  Requests are double-buffered: the next
-    # request's inputs stream in on a copy stream while the current one compresses and
-    # decodes (two device input sets, one decode graph per set); the timed region spans the
-    # first copy to the last read-back, so every step's transfers are inside it.
+    # decode-step attention outputs + budgets).  Q, K and the decode inputs are copied to the
+    # device; V stays on the host and the compress call's gather reads only its retained and
+    # window rows (layer_budget per problem) over the host link (ops.compress with a pinned
+    # V).  Requests are double-buffered: the next request's copies stream in on a copy stream
+    # while the current one compresses and decodes (two device input sets, one decode graph
+    # per set), and each request's prompt arrives and is compressed in chunks of layers, so
+    # compression starts once the first chunk has landed; the timed region spans the first
+    # copy to the last read-back, so every step's transfers are inside it.
     qh, kh, vh = q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory()
     dqh, dkh, dvh = dq.cpu().pin_memory(), dk.cpu().pin_memory(), dv.cpu().pin_memory()
     out_h = torch.empty(dg.out.shape, dtype=dg.out.dtype).pin_memory()
     bud_h = torch.empty(cache.budgets.shape, dtype=torch.int32).pin_memory()
-    h2d = sum(x.numel() * x.element_size() for x in (qh, kh, vh, dqh, dkh, dvh))
+    v_rows_read = P * LB * d * vh.element_size()  # the gather's zero-copy reads of V
+    h2d = sum(x.numel() * x.element_size() for x in (qh, kh, dqh, dkh, dvh)) + v_rows_read
     d2h = out_h.numel() * out_h.element_size() + bud_h.numel() * 4
-    sets = [(q, k, v, dq, dk, dv), tuple(torch.empty_like(x) for x in (q, k, v, dq, dk, dv))]
-    graphs = [graph, capture(*sets[1][3:])]
+    del v
+    sets = [(q, k, dq, dk, dv), tuple(torch.empty_like(x) for x in (q, k, dq, dk, dv))]
+    graphs = [graph, capture(*sets[1][2:])]
     copy_st = torch.cuda.Stream(device=dev)
     comp_st = torch.cuda.current_stream()
     copied = [torch.cuda.Event(), torch.cuda.Event()]
     done = [torch.cuda.Event(), torch.cuda.Event()]
+    nch = 4 if L % 4 == 0 else 1  # layer chunks per request
+    lc = L // nch
+    chunk_in = [[torch.cuda.Event() for _ in range(nch)] for _ in range(2)]
+
+    probe = [] if os.environ.get("ADAKV_E2E_PROBE") else None  # (diagnostic) event timeline
+
+    def mark(tag, stream):
+        if probe is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            probe.append((tag, e))
 
     def h2d_into(i):
         with torch.cuda.stream(copy_st):
             copy_st.wait_event(done[i])  # the set's previous request has finished with it
-            for dst, src in zip(sets[i], (qh, kh, vh, dqh, dkh, dvh)):
+            mark(f"copy{i}+", copy_st)
+            for c in range(nch):
+                for dst, src in zip(sets[i][:2], (qh, kh)):
+                    dst[c * lc:(c + 1) * lc].copy_(src[c * lc:(c + 1) * lc], non_blocking=True)
+                chunk_in[i][c].record(copy_st)
+            for dst, src in zip(sets[i][2:], (dqh, dkh, dvh)):
                 dst.copy_(src, non_blocking=True)
             copied[i].record(copy_st)
+            mark(f"copy{i}-", copy_st)
 
     def e2e_run(nreq):
         for i in range(2):
@@ -453,10 +476,17 @@ def run_ours(args, cfg):
             i = r & 1
             if r + 1 < nreq:
                 h2d_into(i ^ 1)
+            qi, ki = sets[i][:2]
+            mark(f"req{r}", comp_st)
+            for c in range(nch):
+                comp_st.wait_event(chunk_in[i][c])
+                sl = slice(c * lc, (c + 1) * lc)
+                PL.compress_model(qi[sl], ki[sl], vh[sl], LB, reserve=reserve, out=cache, first_layer=c * lc)
+            mark("compressed", comp_st)
             comp_st.wait_event(copied[i])
-            qi, ki, vi = sets[i][:3]
-            PL.compress_model(qi, ki, vi, LB, reserve=reserve, out=cache)
+            mark("decode+", comp_st)
             graphs[i].replay()
+            mark("decode-", comp_st)
             done[i].record(comp_st)
             out_h.copy_(dg.out, non_blocking=True)
             bud_h.copy_(cache.budgets, non_blocking=True)
@@ -472,6 +502,9 @@ def run_ours(args, cfg):
     t1.record(comp_st)
     torch.cuda.synchronize()
     e2e_ms = t0.elapsed_time(t1) / ne2e
+    if probe:
+        print("e2e timeline (ms from start): " + " ".join(f"{tg}@{t0.elapsed_time(e):.1f}" for tg, e in probe
+                                                          if t0.elapsed_time(e) >= 0), file=sys.stderr)
     if ws > 1:
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

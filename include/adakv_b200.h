@@ -100,6 +100,10 @@ int adakv_abi_version(void);
  * 1 = tcgen05 tensor-core kernel (default), 0 = the generic SIMT kernel.  Returns the
  * previous setting.  Both compute the same function; this exists for A/B checks. */
 int adakv_set_tensor_core_scoring(int enabled);
+/* Device address of a pinned (page-locked) host buffer, for the arguments documented as
+ * accepting one (adakv_compress's v).  ADAKV_INVALID_ARGUMENT if `host` is not pinned host
+ * memory mapped into the device's address space. */
+adakv_status adakv_host_device_pointer(const void* host, void** device_ptr);
 /* Reads back (synchronously) the device error word latched in a workspace. */
 adakv_status adakv_workspace_status(const void* workspace, adakv_stream_t stream);
 
@@ -120,6 +124,11 @@ adakv_status adakv_workspace_status(const void* workspace, adakv_stream_t stream
  *   budgets          DEVICE int32 [P*G] outside budget per group (EvictLayerResult::allocation)
  *   group_scores     DEVICE [P*G*n_o] f32 (f64 for ADAKV_F64) or NULL (EvictLayerResult::scores)
  *   keep             DEVICE uint8 [P*G*n_o] or NULL (EvictLayerResult::decision, group leaders)
+ *   v                may also be a device-accessible address of pinned HOST memory (see
+ *                    adakv_host_device_pointer): V is read only by the final gather, for the
+ *                    retained and window rows (layer_budget rows per problem), so a prompt
+ *                    whose V lives on the host crosses the host link for those rows only
+ *                    (k and q are read in full by the scoring and must be in device memory)
  * ------------------------------------------------------------------------- */
 adakv_status adakv_compress(adakv_dtype dtype, const adakv_layer_shape* shape,
                             const adakv_policy_config* cfg, int64_t layer_budget,

@@ -78,6 +78,7 @@ def _sig(L):
     L.adakv_set_tensor_core_scoring.argtypes = [C.c_int]
     L.adakv_set_tensor_core_scoring.restype = C.c_int
     L.adakv_workspace_status.argtypes = [VP, VP]
+    L.adakv_host_device_pointer.argtypes = [VP, C.POINTER(VP)]
     L.adakv_set_decode_overlap.argtypes = [C.c_int]
     L.adakv_set_decode_overlap.restype = C.c_int
     L.adakv_compress.argtypes = [S, C.POINTER(LayerShape), C.POINTER(PolicyConfig), I64, VP, VP, VP, VP, I64,

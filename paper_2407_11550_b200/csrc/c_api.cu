@@ -504,6 +504,18 @@ adakv_status adakv_decode(adakv_dtype dtype, int64_t problems, int64_t q_heads, 
                          overlap, st);
 }
 
+adakv_status adakv_host_device_pointer(const void* host, void** device_ptr) {
+    if (!host || !device_ptr) return fail(ADAKV_INVALID_ARGUMENT, "host_device_pointer: null argument");
+    cudaPointerAttributes at{};
+    const cudaError_t e = cudaPointerGetAttributes(&at, host);
+    if (e != cudaSuccess || at.type != cudaMemoryTypeHost || at.devicePointer == nullptr) {
+        cudaGetLastError();
+        return fail(ADAKV_INVALID_ARGUMENT, "host_device_pointer: not pinned host memory mapped into the device");
+    }
+    *device_ptr = at.devicePointer;
+    return ADAKV_OK;
+}
+
 int adakv_set_decode_overlap(int enabled) {
     const int prev = decode_overlap_enabled() ? 1 : 0;
     g_decode_overlap.store(enabled ? 1 : 0);

@@ -53,6 +53,10 @@ constexpr float kEScaleLog2 = 16.f;               // E carries a 2^16 scale (fp1
 #ifndef ADAKV_PASS2_POLY
 #define ADAKV_PASS2_POLY 0
 #endif
+#ifndef ADAKV_PASS1_POLY
+#define ADAKV_PASS1_POLY 2
+#endif
+constexpr int kPass1Poly = ADAKV_PASS1_POLY;      // pass-1 exp2 split (see exp2_mixed)
 constexpr int kPass2Poly = ADAKV_PASS2_POLY;      // pass-2 exp2 split (see exp2_mixed)
 
 struct __align__(1024) Smem {
@@ -441,7 +445,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                         // 2 of every 8 exp2 on the FMA pipe (polynomial), 6 on MUFU: measured
                         // fastest split (debug 64: MUFU only)
                         if (prm.debug & 64) exp2_mixed<32, 0>(v, 32);
-                        else exp2_mixed<32, 2>(v, 32);
+                        else exp2_mixed<32, kPass1Poly>(v, 32);
                         uint64_t a0 = pk(0.f, 0.f), a1 = pk(0.f, 0.f);
 #pragma unroll
                         for (int c = 0; c < 32; c += 4) {

@@ -98,17 +98,38 @@ class CompressedCache:
         return self.k[s:s + n], self.v[s:s + n]
 
 
+def host_device_pointer(t: torch.Tensor) -> C.c_void_p:
+    """Device address of a pinned, contiguous CPU tensor (adakv_host_device_pointer)."""
+    if t.is_cuda or not t.is_pinned():
+        raise L.InvalidArgument(1, "host buffers must be pinned CPU tensors (tensor.pin_memory())")
+    if not t.is_contiguous():
+        raise L.InvalidArgument(1, "tensors must be contiguous")
+    dp = C.c_void_p()
+    L.check(L.lib().adakv_host_device_pointer(C.c_void_p(t.data_ptr()), C.byref(dp)))
+    return dp
+
+
 def compress(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layer_budget: int, kind="ada_snapkv",
              pool_kernel=7, alpha=0.2, sink_tokens=4, scale=True, reserve=0, layer_budgets=None,
              return_scores=False, return_keep=False, out: CompressedCache | None = None,
-             ws: torch.Tensor | None = None) -> CompressedCache:
+             ws: torch.Tensor | None = None, first_problem: int = 0) -> CompressedCache:
     """evict_layer (policies.hpp:204-293) for P problems at once.
 
     q [P, H, m, d]; k, v [P, G, n, d] with the observation window in the last m rows.
+    v may be a pinned CPU tensor: only the retained and window rows (layer_budget per
+    problem) are then read, by the gather, straight from host memory.
     layer_budget counts unique KV entries per problem, window included.
     layer_budgets: optional int64 CUDA tensor [P] (per-problem budgets, pyramid kinds).
+    first_problem: with `out` and uniform budgets, write these P problems as problems
+    [first_problem, first_problem + P) of `out` (a model's layers compressed in chunks, e.g. as
+    their inputs arrive); the rows land exactly where one call over all problems puts them.
     """
-    _need_cuda(q, k, v)
+    _need_cuda(q, k)
+    if v.is_cuda:
+        _need_cuda(v)
+        v_ptr = _p(v)
+    else:
+        v_ptr = host_device_pointer(v)
     P, H, m, d = q.shape
     P2, G, n, d2 = k.shape
     if P2 != P or d2 != d or v.shape != k.shape or k.dtype != q.dtype or v.dtype != q.dtype:
@@ -137,14 +158,27 @@ def compress(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layer_budget: in
             P=P, H=H, G=G, m=m, d=d, reserve=reserve, layer_budget=lbmax,
             scores=torch.empty((P, G, n_o), dtype=acc_dtype, device=dev) if return_scores else None,
             keep=torch.empty((P, G, n_o), dtype=torch.uint8, device=dev) if return_keep else None)
+    p0 = int(first_problem)
+    row0 = 0
+    if p0:
+        if out is None or layer_budgets is not None or p0 < 0 or p0 + P > out.P:
+            raise L.InvalidArgument(1, "compress: first_problem needs `out` with room and uniform budgets")
+        row0 = p0 * (layer_budget + G * reserve)
+
+    def at(t, off):
+        return None if t is None else C.c_void_p(t.data_ptr() + off * t.element_size())
+
     nbytes = C.c_size_t()
     L.check(lib.adakv_compress_workspace(dt, C.byref(shape), C.byref(cfg), C.byref(nbytes)))
     if ws is None:
         ws = workspace(nbytes.value, dev, "compress")
     L.check(lib.adakv_compress(dt, C.byref(shape), C.byref(cfg), int(layer_budget), _p(layer_budgets), _p(q),
-                               _p(k), _p(v), int(reserve), _p(out.k), _p(out.v), _p(out.seg_start),
-                               _p(out.seqlens), _p(out.budgets), _p(out.scores), _p(out.keep), _p(ws),
+                               _p(k), v_ptr, int(reserve), at(out.k, row0 * d), at(out.v, row0 * d),
+                               at(out.seg_start, p0 * G), at(out.seqlens, p0 * G), at(out.budgets, p0 * G),
+                               at(out.scores, p0 * G * n_o), at(out.keep, p0 * G * n_o), _p(ws),
                                ws.numel(), _stream()))
+    if row0:  # the library laid the segments out from row 0 of the planes it was given
+        out.seg_start[p0 * G:(p0 + P) * G] += row0
     return out
 
 

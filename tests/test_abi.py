@@ -69,3 +69,12 @@ def test_python_ops_refuse_cpu_tensors():
     k = torch.zeros(1, 2, 10, 8)
     with pytest.raises(A.InvalidArgument):
         A.compress(q, k, k, 8)
+
+
+def test_host_v_must_be_pinned_cpu_tensor():
+    """ops.compress accepts a host V only as a pinned, contiguous CPU tensor; anything else
+    raises the reference's invalid_argument type before the library is called."""
+    import torch
+    from paper_2407_11550_b200 import InvalidArgument, ops
+    with pytest.raises(InvalidArgument):
+        ops.host_device_pointer(torch.zeros(4, 4))  # not pinned (no CUDA here: cannot pin)

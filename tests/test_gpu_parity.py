@@ -273,6 +273,58 @@ def test_compress_bf16_llama_identical_scores(dev, oracle_mod, kind):
         assert np.abs(out.scores[p, g].double().cpu().numpy() - ref).max() <= 1e-4 * ref.max()
 
 
+def test_compress_host_resident_v_identical(dev):
+    """V given as a pinned host tensor (the gather reads its retained and window rows over the
+    host link): every output -- budgets, decisions and both cache planes -- is byte-identical
+    to the device-V call; unpinned host memory is refused by the C ABI."""
+    P, H, G, m, n_o, d = 2, 32, 8, 32, 4064, 128
+    LB = 1024 * G
+    q, k, v = planted_layer(P, H, G, n_o, m, d, seed=5, dtype=torch.bfloat16, device=dev)
+    ref = A.compress(q, k, v, LB, reserve=8, return_keep=True)
+    vh = v.cpu().pin_memory()
+    got = A.compress(q, k, vh, LB, reserve=8, return_keep=True)
+    torch.cuda.synchronize()
+    for name in ("budgets", "seg_start", "seqlens", "keep"):
+        assert torch.equal(getattr(got, name), getattr(ref, name)), name
+    for p in range(P):  # the segments' rows (the reserve rows past them are unwritten)
+        for g in range(G):
+            (kr, vr), (kg, vg) = ref.segment(p, g), got.segment(p, g)
+            assert torch.equal(kg, kr) and torch.equal(vg, vr)
+    with pytest.raises(A.InvalidArgument):
+        A.compress(q, k, v.cpu(), LB)
+    import ctypes as C
+    from paper_2407_11550_b200 import _lib
+    plain = torch.zeros(16)
+    dp = C.c_void_p()
+    assert _lib.lib().adakv_host_device_pointer(C.c_void_p(plain.data_ptr()), C.byref(dp)) == 1  # invalid_argument
+
+
+def test_compress_in_layer_chunks_identical(dev):
+    """A model compressed in chunks of layers (pipeline.compress_model first_layer, as the
+    e2e bench does while later layers are still arriving) fills the same cache as one call."""
+    from paper_2407_11550_b200 import pipeline as PL
+    Lyr, H, G, m, n_o, d = 4, 32, 8, 32, 1000, 128
+    LB = 256 * G
+    q, k, v = planted_layer(Lyr, H, G, n_o, m, d, seed=9, dtype=torch.bfloat16, device=dev)
+    q, k, v = q.reshape(Lyr, 1, H, m, d), k.reshape(Lyr, 1, G, n_o + m, d), v.reshape(Lyr, 1, G, n_o + m, d)
+    one = PL.compress_model(q, k, v, LB, reserve=4)
+    ch = PL.compress_model(q, k, v, LB, reserve=4)
+    ch.k.zero_()
+    ch.seg_start.zero_()
+    for l0 in (2, 0, 3, 1):  # any order
+        PL.compress_model(q[l0:l0 + 1], k[l0:l0 + 1], v.cpu().pin_memory()[l0:l0 + 1], LB, reserve=4, out=ch,
+                          first_layer=l0)
+    torch.cuda.synchronize()
+    for name in ("budgets", "seg_start", "seqlens"):
+        assert torch.equal(getattr(ch, name), getattr(one, name)), name
+    for p in range(Lyr):
+        for g in range(G):
+            (k1, v1), (k2, v2) = one.segment(p, g), ch.segment(p, g)
+            assert torch.equal(k1, k2) and torch.equal(v1, v2)
+    with pytest.raises(A.InvalidArgument):
+        PL.compress_model(q[3:], k[3:], v[3:], LB, reserve=4, out=ch, first_layer=4)
+
+
 def test_compress_per_problem_budgets(dev, oracle_mod):
     """pyramid schedule (budget.hpp:169-191): per-problem layer budgets in one launch."""
     O = oracle_mod
