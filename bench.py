@@ -558,7 +558,9 @@ def run_ours(args, cfg):
         "roofline": roof, "clocks": clk.result, "gpu_launches": launches,
         "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms, 3), "requests": ne2e,
-                "overlap": "next request's H2D on a copy stream during the current compress + decode"},
+                "overlap": "next request's Q/K/decode-input H2D on a copy stream during the current compress + "
+                           "decode; layers compressed in 4 chunks as they land; V read in place from pinned host "
+                           "memory (retained + window rows only, counted in h2d_bytes_per_step)"},
         "peak_source": src,
     }
     if scal:
