@@ -56,6 +56,10 @@ constexpr int kBlk = 16;
 #ifndef ADAKV_DECODE_W
 #define ADAKV_DECODE_W 8
 #endif
+#ifndef ADAKV_DEC_TRIPLE
+#define ADAKV_DEC_TRIPLE 1
+#endif
+constexpr bool kTriple = ADAKV_DEC_TRIPLE != 0;  // last three blocks of a warp as one step
 constexpr int kMaxWarps = ADAKV_DECODE_W;   // warps per CTA (template parameter W <= kMaxWarps)
 constexpr int kMaxSlots = 3;               // ring depth per warp (runtime <= kMaxSlots; 227 KB smem)
 constexpr int kBoxBytes = kBlk * 256;      // one 16-row box of K (or V): [16 rows][2 halves][128 B]
@@ -444,6 +448,37 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     // softmax over 32 keys, then both PVs -- the two blocks' latency chains overlap.
     int j = 0;
     while (j < nb) {
+        if (kTriple && nb - j == 3 && nslots >= 3) {
+            // exactly three left (a warp of a CTA whose block count is not a multiple of 2W):
+            // one softmax over 48 keys and three S chains in flight instead of a pair + a single
+            int s1 = s, s2;
+            uint32_t ph1 = sphase, ph2;
+            advance(s1, ph1);
+            s2 = s1;
+            ph2 = ph1;
+            advance(s2, ph2);
+            uint4 kvc[2][4];
+            fetch_k(j + 1, s1, ph1, kvb);
+            fetch_k(j + 2, s2, ph2, kvc);
+            float x[12];
+            scores(j, kva, *reinterpret_cast<float(*)[4]>(&x[0]));
+            scores(j + 1, kvb, *reinterpret_cast<float(*)[4]>(&x[4]));
+            scores(j + 2, kvc, *reinterpret_cast<float(*)[4]>(&x[8]));
+            softmax(x, 12);
+            uint4 vv[4][2];
+            load_v(s, vv);
+            pv(vv, &x[0]);
+            load_v(s1, vv);
+            pv(vv, &x[4]);
+            load_v(s2, vv);
+            pv(vv, &x[8]);
+            __syncwarp();
+            s = s2;
+            sphase = ph2;
+            advance(s, sphase);
+            j += 3;  // the last blocks of this warp: nothing left to issue
+            continue;
+        }
         if (j + 1 < nb) {
             int s1 = s;
             uint32_t ph1 = sphase;

@@ -514,6 +514,39 @@ def test_decode_long_segments_ring_rounds(dev, oracle_mod):
         assert torch.equal(segs[3][0][-1], kn[0, 3]) and torch.equal(segs[3][1][-1], vn[0, 3])
 
 
+def test_decode_three_block_warps_vs_oracle(dev, oracle_mod):
+    """Segment lengths that give warps exactly three 16-row blocks (the fused three-block step)
+    or a pair followed by a single, with appends, against the fp64 oracle."""
+    from paper_2407_11550_b200.ops import CompressedCache
+    O = oracle_mod
+    P, H, G, d, reserve = 1, 32, 8, 128, 4
+    lens = np.array([3455, 2879, 2300, 1000, 47, 3456 + 16 * 9 - 1, 3000, 2049], dtype=np.int32)
+    caps = lens + reserve
+    starts = np.concatenate([[0], np.cumsum(caps)[:-1]]).astype(np.int32)
+    rows = int(caps.sum())
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(21)
+    kp = (torch.randn((rows, d), generator=gen, device=dev) * 0.5).to(torch.bfloat16)
+    vp = torch.randn((rows, d), generator=gen, device=dev).to(torch.bfloat16)
+    cache = CompressedCache(k=kp, v=vp, seg_start=torch.as_tensor(starts, device=dev),
+                            seqlens=torch.as_tensor(lens, device=dev), budgets=torch.as_tensor(lens, device=dev),
+                            P=P, H=H, G=G, m=0, d=d, reserve=reserve, layer_budget=int(lens.max()))
+    for step in range(2):
+        qd = torch.randn((P, H, d), generator=gen, device=dev).to(torch.bfloat16)
+        kn = torch.randn((P, G, d), generator=gen, device=dev).to(torch.bfloat16)
+        vn = torch.randn((P, G, d), generator=gen, device=dev).to(torch.bfloat16)
+        o = A.decode(qd, cache, kn, vn)
+        segs = [cache.segment(0, g) for g in range(G)]
+        assert [sg[0].shape[0] for sg in segs] == (lens + step + 1).tolist()
+        off = np.concatenate([[0], np.cumsum([sg[0].shape[0] for sg in segs])])
+        ref = O.decode_attention(qd[0].double().cpu().numpy(), torch.cat([sg[0] for sg in segs]).double().cpu().numpy(),
+                                 torch.cat([sg[1] for sg in segs]).double().cpu().numpy(), off)
+        err = np.abs(o[0].double().cpu().numpy() - ref).max()
+        assert err <= 2e-2 and err <= 1e-2 * max(np.abs(ref).max(), 1e-3) + 4e-3, (step, err)
+        for g in range(G):
+            assert torch.equal(segs[g][0][-1], kn[0, g]) and torch.equal(segs[g][1][-1], vn[0, g])
+
+
 def test_decode_umma_variant_vs_oracle(dev, oracle_mod):
     """The opt-in tcgen05 decode (decode_umma.cu): multi-step appends over long segments."""
     O = oracle_mod
