@@ -490,12 +490,20 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         uint32_t gt = 0, eq = 0;
         if (mode == MODE_THRESH) {
             const KT T = seg_T[s];
-            for (int64_t base = a; base < b; base += 32) {
-                const int64_t e = base + lane;
-                KT u = 0;
-                if (e < b) u = key_at(e);
-                gt += __popc(__ballot_sync(0xffffffffu, e < b && u > T));
-                eq += __popc(__ballot_sync(0xffffffffu, e < b && u == T));
+            // four chunks' loads in flight before any compare
+            for (int64_t base = a; base < b; base += 128) {
+                KT u[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int64_t e = base + c * 32 + lane;
+                    u[c] = e < b ? key_at(e) : KT(0);
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const bool ok = base + c * 32 + lane < b;
+                    gt += __popc(__ballot_sync(0xffffffffu, ok && u[c] > T));
+                    eq += __popc(__ballot_sync(0xffffffffu, ok && u[c] == T));
+                }
             }
         } else if (mode == MODE_ALL) {
             gt = uint32_t(b - a);
@@ -607,28 +615,43 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
             // 32-bit element offsets from the warp's range start (ranges fit 32 bits)
             const int len = int(b - a);
             const int pos0 = int(a - off_s);
-            for (int o = 0; o < len; o += 32) {
-                const int j = o + lane;
-                const bool valid = j < len;
-                const int pos = pos0 + j;
-                bool keep = false;
-                if (mode == MODE_THRESH) {
-                    KT u = 0;
-                    if (valid) u = key_at(a + j);
-                    const bool is_eq = valid && u == T;
-                    const unsigned beq = __ballot_sync(0xffffffffu, is_eq);
-                    const int64_t eqr = run_eq + __popc(beq & lt);
-                    keep = valid && (u > T || (is_eq && eqr < need));
-                    run_eq += __popc(beq);
-                } else if (mode == MODE_ALL) {
-                    keep = valid;
-                } else if (mode == MODE_STREAM) {
-                    keep = valid && (pos < sink || pos >= recent_lo);
-                }
+            auto emit = [&](int j, bool valid, bool keep) {
                 const unsigned bk = __ballot_sync(0xffffffffu, keep);
-                if (keep && kp) kp[run_kept + __popc(bk & lt)] = int32_t(pos);
+                if (keep && kp) kp[run_kept + __popc(bk & lt)] = int32_t(pos0 + j);
                 if (valid && keep_out) keep_out[a + j] = keep ? 1 : 0;
                 run_kept += __popc(bk);
+            };
+            if (mode == MODE_THRESH) {
+                // four chunks' key loads issued ahead of the stores (which may alias them)
+                for (int o = 0; o < len; o += 128) {
+                    KT u[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int j = o + c * 32 + lane;
+                        u[c] = j < len ? key_at(a + j) : KT(0);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        if (o + c * 32 >= len) break;  // warp-uniform
+                        const int j = o + c * 32 + lane;
+                        const bool valid = j < len;
+                        const bool is_eq = valid && u[c] == T;
+                        const unsigned beq = __ballot_sync(0xffffffffu, is_eq);
+                        const int64_t eqr = run_eq + __popc(beq & lt);
+                        emit(j, valid, valid && (u[c] > T || (is_eq && eqr < need)));
+                        run_eq += __popc(beq);
+                    }
+                }
+            } else {
+                for (int o = 0; o < len; o += 32) {
+                    const int j = o + lane;
+                    const bool valid = j < len;
+                    const int pos = pos0 + j;
+                    bool keep = false;
+                    if (mode == MODE_ALL) keep = valid;
+                    else if (mode == MODE_STREAM) keep = valid && (pos < sink || pos >= recent_lo);
+                    emit(j, valid, keep);
+                }
             }
         }
     }
