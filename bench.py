@@ -256,14 +256,8 @@ def decode_batch_scaling(dev, H, G, d, L, budget_rows, batches=(1, 8), steps=4, 
             with torch.cuda.graph(g, stream=st):
                 for s in range(steps):
                     for l in range(L):
-                        seg = l * B * G
-                        A._lib.check(lib.adakv_decode(
-                            2, B, H, G, d, 1, C.c_void_p(dq[s, l].data_ptr()), C.c_void_p(kp.data_ptr()),
-                            C.c_void_p(vp.data_ptr()), rows, C.c_void_p(cache.seg_start.data_ptr() + 4 * seg),
-                            C.c_void_p(cache.seqlens.data_ptr() + 4 * seg), int(caps.max()),
-                            C.c_void_p(dk[s, l].data_ptr()), C.c_void_p(dk[s, l].data_ptr()),  # k_new, v_new
-                            C.c_void_p(dg.out[l].data_ptr()), C.c_void_p(dg.ws.data_ptr()), dg.ws.numel(),
-                            C.c_void_p(st.cuda_stream)))
+                        PL.decode_layer(lib, cache, l, B, dq[s, l], dk[s, l], dk[s, l], dg.out[l], dg.ws,
+                                        int(caps.max()), C.c_void_p(st.cuda_stream), chained=s > 0 or l > 0)
         torch.cuda.current_stream().wait_stream(st)
         torch.cuda.synchronize()
         g.replay()  # warm
@@ -326,23 +320,15 @@ def run_ours(args, cfg):
     lib = A.lib()
     import ctypes as C
     st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-    A._lib.check(lib.adakv_decode(2, B, H, G, d, 1, C.c_void_p(dq[0, 0].data_ptr()), C.c_void_p(cache.k.data_ptr()),
-                                  C.c_void_p(cache.v.data_ptr()), cache.k.shape[0], C.c_void_p(cache.seg_start.data_ptr()),
-                                  C.c_void_p(cache.seqlens.data_ptr()), max_rows, None, None,
-                                  C.c_void_p(dg.out[0].data_ptr()), C.c_void_p(dg.ws.data_ptr()), dg.ws.numel(), st))
+    PL.decode_layer(lib, cache, 0, B, dq[0, 0], None, None, dg.out[0], dg.ws, max_rows, st, chained=False)
     torch.cuda.synchronize()
 
     def decode_launches(dq_, dk_, dv_):
         stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         for s in range(S):
             for l in range(L):
-                seg = l * B * G
-                A._lib.check(lib.adakv_decode(
-                    2, B, H, G, d, 1, C.c_void_p(dq_[s, l].data_ptr()), C.c_void_p(cache.k.data_ptr()),
-                    C.c_void_p(cache.v.data_ptr()), cache.k.shape[0], C.c_void_p(cache.seg_start.data_ptr() + 4 * seg),
-                    C.c_void_p(cache.seqlens.data_ptr() + 4 * seg), max_rows, C.c_void_p(dk_[s, l].data_ptr()),
-                    C.c_void_p(dv_[s, l].data_ptr()), C.c_void_p(dg.out[l].data_ptr()), C.c_void_p(dg.ws.data_ptr()),
-                    dg.ws.numel(), stream))
+                PL.decode_layer(lib, cache, l, B, dq_[s, l], dk_[s, l], dv_[s, l], dg.out[l], dg.ws, max_rows,
+                                stream, chained=s > 0 or l > 0)
 
     def capture(dq_, dk_, dv_):
         g_ = torch.cuda.CUDAGraph()

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define ADAKV_B200_ABI_VERSION 1
+#define ADAKV_B200_ABI_VERSION 2
 
 typedef struct CUstream_st* adakv_stream_t; /* == cudaStream_t */
 
@@ -104,8 +104,27 @@ int adakv_set_tensor_core_scoring(int enabled);
  * accepting one (adakv_compress's v).  ADAKV_INVALID_ARGUMENT if `host` is not pinned host
  * memory mapped into the device's address space. */
 adakv_status adakv_host_device_pointer(const void* host, void** device_ptr);
-/* Reads back (synchronously) the device error word latched in a workspace. */
+/* Reads back (synchronously) the device error word latched in a workspace and maps it onto
+ * the reference's exception (message included):
+ *   non-finite K/V               -> ADAKV_INVALID_ARGUMENT "LayerCache: non-finite entry"
+ *                                   (LayerCache::validate, attention.hpp:76-83)
+ *   budget outside floor/capacity -> ADAKV_INVALID_ARGUMENT (policies.hpp:229-231, budget.hpp:48-59)
+ *   append past a segment's capacity -> ADAKV_INVALID_ARGUMENT "append_kv: capacity exhausted"
+ * Every workspace starts with this 256-byte error header; it is cleared by the entry points
+ * that take the workspace as their first stage (compress, window_scores, segmented_select)
+ * and accumulates otherwise (decode, append), so one read after a decode loop reports any
+ * step that overflowed.  adakv_clear_workspace_status() resets it. */
 adakv_status adakv_workspace_status(const void* workspace, adakv_stream_t stream);
+adakv_status adakv_clear_workspace_status(void* workspace, adakv_stream_t stream);
+
+/* LayerCache::validate (attention.hpp:76-83) on the device: latches ERR_NONFINITE in the
+ * workspace error word if any of the n elements at `data` (dtype) is NaN or +-Inf.  The
+ * compress path checks, for free, every K entry that reaches a window row's softmax
+ * statistics (a NaN or +Inf logit) and every K/V row the gather copies (retained + window
+ * rows); a caller that needs the reference's full check of the prompt cache (every K and V
+ * entry, including evicted rows) runs this over k and v first: one extra HBM read. */
+adakv_status adakv_validate_finite(adakv_dtype dtype, const void* data, int64_t n, void* workspace,
+                                   adakv_stream_t stream);
 
 /* ----------------------------------------------------------------------------
  * Full single-layer eviction pass for P problems:
@@ -121,6 +140,8 @@ adakv_status adakv_workspace_status(const void* workspace, adakv_stream_t stream
  *   reserve          extra rows per segment for decode appends (capacity = budget_g + m + reserve)
  *   k_cache,v_cache  output planes, adakv_cache_rows() rows of d elements (same dtype as k)
  *   seg_start,seqlens  DEVICE int32 [P*G]
+ *   seg_cap          DEVICE int32 [P*G] or NULL: each segment's capacity in rows
+ *                    (budget_g + m + reserve); decode / append refuse to write past it
  *   budgets          DEVICE int32 [P*G] outside budget per group (EvictLayerResult::allocation)
  *   group_scores     DEVICE [P*G*n_o] f32 (f64 for ADAKV_F64) or NULL (EvictLayerResult::scores)
  *   keep             DEVICE uint8 [P*G*n_o] or NULL (EvictLayerResult::decision, group leaders)
@@ -134,7 +155,7 @@ adakv_status adakv_compress(adakv_dtype dtype, const adakv_layer_shape* shape,
                             const adakv_policy_config* cfg, int64_t layer_budget,
                             const int64_t* layer_budgets, const void* q, const void* k,
                             const void* v, int64_t reserve, void* k_cache, void* v_cache,
-                            int32_t* seg_start, int32_t* seqlens, int32_t* budgets,
+                            int32_t* seg_start, int32_t* seqlens, int32_t* seg_cap, int32_t* budgets,
                             void* group_scores, uint8_t* keep, void* workspace,
                             size_t workspace_bytes, adakv_stream_t stream);
 adakv_status adakv_compress_workspace(adakv_dtype dtype, const adakv_layer_shape* shape,
@@ -199,14 +220,16 @@ adakv_status adakv_segmented_select_workspace(int64_t problems, int64_t segments
 /* ----------------------------------------------------------------------------
  * Stage 3 -- compaction gather (K3 copy half): for every (p, g) copy the kept
  * outside rows (kept_pos from adakv_segmented_select) then the m window rows into
- * the output planes; writes seg_start / seqlens.  Bit-exact copy, 16-byte vectors.
+ * the output planes; writes seg_start / seqlens (and seg_cap if not NULL).  Bit-exact copy,
+ * 16-byte vectors; the copied rows are checked for non-finite entries (ERR_NONFINITE in the
+ * error word at `workspace`, which may be NULL to skip the latch).
  * layer_budget / layer_budgets as for adakv_compress (they fix each problem's row base).
  * ------------------------------------------------------------------------- */
 adakv_status adakv_gather(adakv_dtype dtype, const adakv_layer_shape* shape, int64_t layer_budget,
                           const int64_t* layer_budgets, const void* k, const void* v,
                           const int32_t* budgets, const int32_t* kept_pos, int64_t kept_stride,
                           int64_t reserve, void* k_cache, void* v_cache, int32_t* seg_start,
-                          int32_t* seqlens, adakv_stream_t stream);
+                          int32_t* seqlens, int32_t* seg_cap, void* workspace, adakv_stream_t stream);
 
 /* ----------------------------------------------------------------------------
  * Decode (K4 split-K varlen flash-decoding + K5 append):
@@ -216,45 +239,52 @@ adakv_status adakv_gather(adakv_dtype dtype, const adakv_layer_shape* shape, int
  *   q          DEVICE [P, H, d]
  *   k_cache, v_cache  the planes (cache_rows rows of d elements each; the segments'
  *              seg_start offsets index into them)
+ *   seg_cap    DEVICE int32 [P*G]: capacity of each segment in rows (from adakv_compress)
  *   k_new,v_new  DEVICE [P, G, d] or NULL: appended at row seqlens (the new token's
  *              own K/V, attended in the same step); seqlens is then incremented on the
- *              device.  Requires seqlens < capacity (caller-reserved).
+ *              device.  A segment already at capacity is not written: its attention runs
+ *              over the existing rows and ERR_CAPACITY is latched in the workspace error
+ *              word (append_kv's std::invalid_argument through adakv_workspace_status).
  *   out        DEVICE [P, H, d] (same dtype as q)
- * Ordering: back-to-back decodes of DIFFERENT segments on one stream (the layers of a
- * model-wide plane) overlap through programmatic dependent launch -- the next call's
- * cache rows stream in while the previous call finishes.  The library tracks its own
- * launches per stream and never overlaps a decode with its own compress / gather /
- * append_kv or with a decode of the same segments.  A caller kernel enqueued directly
- * before adakv_decode must not write that call's cache rows, seg_start or seqlens, or
- * the caller disables the overlap with adakv_set_decode_overlap(0)
- * (env ADAKV_DECODE_OVERLAP=0).
+ *   flags      ADAKV_DECODE_CHAINED: the caller guarantees that the kernel enqueued directly
+ *              before this call on `stream` is an adakv_decode of OTHER segments and writes
+ *              nothing this call reads (its cache rows, seg_start, seg_cap, seqlens, q, k_new,
+ *              v_new) -- the layers of one decode step, enqueued back to back.  The call
+ *              then overlaps its predecessor through programmatic dependent launch (its
+ *              cache rows stream in while the previous layer finishes; q is still read only
+ *              after the predecessor has completed).  0: plain stream order.
  * ------------------------------------------------------------------------- */
+#define ADAKV_DECODE_CHAINED 1u
 adakv_status adakv_decode(adakv_dtype dtype, int64_t problems, int64_t q_heads,
                           int64_t kv_groups, int64_t head_dim, int32_t scale, const void* q,
                           void* k_cache, void* v_cache, int64_t cache_rows, const int32_t* seg_start,
-                          int32_t* seqlens, int64_t max_rows, const void* k_new,
+                          const int32_t* seg_cap, int32_t* seqlens, int64_t max_rows, const void* k_new,
                           const void* v_new, void* out, void* workspace, size_t workspace_bytes,
-                          adakv_stream_t stream);
+                          uint32_t flags, adakv_stream_t stream);
 /* max_rows: upper bound of any segment length during this call (grid sizing; the
  * launch covers ceil(max_rows / chunk) splits so the call can live in a CUDA graph). */
 adakv_status adakv_decode_workspace(int64_t problems, int64_t q_heads, int64_t kv_groups,
                                     int64_t head_dim, int64_t max_rows, size_t* bytes);
 
-/* Enables (1, default) or disables (0) the decode overlap described above; returns the
- * previous setting. */
+/* Disables (0) the overlap of ADAKV_DECODE_CHAINED calls (they then run in plain stream
+ * order; for A/B measurements); returns the previous setting (default 1). */
 int adakv_set_decode_overlap(int enabled);
 
-/* append_kv (attention.hpp:126-134) alone: one row per segment listed. */
+/* append_kv (attention.hpp:126-134) alone: one row per segment listed.  A segment at
+ * capacity (seg_cap) is left untouched and ERR_CAPACITY is latched in `workspace`'s error
+ * word (>= 256 bytes). */
 adakv_status adakv_append_kv(adakv_dtype dtype, int64_t segments, int64_t head_dim,
                              void* k_cache, void* v_cache, const int32_t* seg_start,
-                             int32_t* seqlens, const void* k_new, const void* v_new,
-                             adakv_stream_t stream);
+                             const int32_t* seg_cap, int32_t* seqlens, const void* k_new,
+                             const void* v_new, void* workspace, adakv_stream_t stream);
 /* append_kv (attention.hpp:126-134) repeated `rows` times per segment (e.g. the question
  * tokens appended after a question-agnostic compression): k_new / v_new DEVICE
- * [segments, rows, d]; seqlens[s] += rows.  Requires seqlens + rows <= capacity. */
+ * [segments, rows, d]; seqlens[s] += rows.  A segment without `rows` free rows is left
+ * untouched and ERR_CAPACITY is latched, as for adakv_append_kv. */
 adakv_status adakv_append_rows(adakv_dtype dtype, int64_t segments, int64_t rows, int64_t head_dim,
-                               void* k_cache, void* v_cache, const int32_t* seg_start, int32_t* seqlens,
-                               const void* k_new, const void* v_new, adakv_stream_t stream);
+                               void* k_cache, void* v_cache, const int32_t* seg_start,
+                               const int32_t* seg_cap, int32_t* seqlens, const void* k_new,
+                               const void* v_new, void* workspace, adakv_stream_t stream);
 
 /* ----------------------------------------------------------------------------
  * Budget integerisation on the device (bit-exact fp64, no FMA contraction).

@@ -617,7 +617,7 @@ inline EvictLayerResult evict_layer(const LayerCache& cache_outside, const Layer
     dev::check(adakv_compress_workspace(ADAKV_F64, &shape, &cfg, &wsb));
     dev::Buffer<std::uint8_t> ws(wsb);
     dev::check(adakv_compress(ADAKV_F64, &shape, &cfg, int64_t(layer_budget), nullptr, dq.get(), dk.get(), dv.get(), 0,
-                              kc.get(), vc.get(), ss.get(), sl.get(), bud.get(), gsc.get(), keep.get(), ws.get(), wsb,
+                              kc.get(), vc.get(), ss.get(), sl.get(), nullptr, bud.get(), gsc.get(), keep.get(), ws.get(), wsb,
                               nullptr));
     dev::check(adakv_workspace_status(ws.get(), nullptr));
     const auto h_bud = bud.download(groups);

@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(PKG, "lib", "libadakv_b200.so")
 F32, F64, BF16 = 0, 1, 2
 KINDS = {"snapkv": 0, "pyramid": 1, "ada_snapkv": 2, "ada_pyramid": 3, "streaming_llm": 4}
 ALLOC_ADAPTIVE, ALLOC_UNIFORM, ALLOC_GIVEN = 0, 1, 2
+DECODE_CHAINED = 1  # adakv_decode flag: the previous kernel on the stream is a decode of other segments
 
 STATUS = {0: "ok", 1: "invalid_argument", 2: "out_of_range", 3: "format_error", 4: "io_error",
           5: "cuda_error", 6: "unsupported", 7: "workspace_too_small"}
@@ -78,11 +79,13 @@ def _sig(L):
     L.adakv_set_tensor_core_scoring.argtypes = [C.c_int]
     L.adakv_set_tensor_core_scoring.restype = C.c_int
     L.adakv_workspace_status.argtypes = [VP, VP]
+    L.adakv_clear_workspace_status.argtypes = [VP, VP]
+    L.adakv_validate_finite.argtypes = [S, VP, I64, VP, VP]
     L.adakv_host_device_pointer.argtypes = [VP, C.POINTER(VP)]
     L.adakv_set_decode_overlap.argtypes = [C.c_int]
     L.adakv_set_decode_overlap.restype = C.c_int
     L.adakv_compress.argtypes = [S, C.POINTER(LayerShape), C.POINTER(PolicyConfig), I64, VP, VP, VP, VP, I64,
-                                 VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP]
+                                 VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP]
     L.adakv_compress_workspace.argtypes = [S, C.POINTER(LayerShape), C.POINTER(PolicyConfig), PSZ]
     L.adakv_cache_rows.argtypes = [C.POINTER(LayerShape), I64, VP, I64]
     L.adakv_cache_rows.restype = I64
@@ -91,11 +94,13 @@ def _sig(L):
     L.adakv_segmented_select.argtypes = [S, I64, I64, PI64, VP, I64, VP, C.POINTER(SelectConfig), VP, VP, VP,
                                          VP, I64, VP, SZ, VP]
     L.adakv_segmented_select_workspace.argtypes = [I64, I64, PSZ]
-    L.adakv_gather.argtypes = [S, C.POINTER(LayerShape), I64, VP, VP, VP, VP, VP, I64, I64, VP, VP, VP, VP, VP]
-    L.adakv_decode.argtypes = [S, I64, I64, I64, I64, I32, VP, VP, VP, I64, VP, VP, I64, VP, VP, VP, VP, SZ, VP]
+    L.adakv_gather.argtypes = [S, C.POINTER(LayerShape), I64, VP, VP, VP, VP, VP, I64, I64, VP, VP, VP, VP, VP, VP,
+                               VP]
+    L.adakv_decode.argtypes = [S, I64, I64, I64, I64, I32, VP, VP, VP, I64, VP, VP, VP, I64, VP, VP, VP, VP, SZ,
+                               C.c_uint32, VP]
     L.adakv_decode_workspace.argtypes = [I64, I64, I64, I64, I64, PSZ]
-    L.adakv_append_kv.argtypes = [S, I64, I64, VP, VP, VP, VP, VP, VP, VP]
-    L.adakv_append_rows.argtypes = [S, I64, I64, I64, VP, VP, VP, VP, VP, VP, VP]
+    L.adakv_append_kv.argtypes = [S, I64, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP]
+    L.adakv_append_rows.argtypes = [S, I64, I64, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP]
     L.adakv_apportion.argtypes = [VP, I64, I64, VP, VP]
     L.adakv_uniform_allocation.argtypes = [I64, I64, VP, VP]
     L.adakv_safeguard_blend.argtypes = [VP, I64, I64, I64, C.c_double, VP, VP]

@@ -16,63 +16,45 @@ namespace adakv_b200 {
 size_t score_window_generic_workspace(adakv_dtype dt, const adakv_layer_shape& s);
 adakv_status score_window_generic(adakv_dtype dt, const adakv_layer_shape& s, int64_t pool_kernel,
                                   int32_t scale, const void* q, const void* k, void* head_scores,
-                                  void* group_scores, void* ws, cudaStream_t stream);
+                                  void* group_scores, void* ws, uint32_t* err, cudaStream_t stream);
 size_t score_window_generic_smem(adakv_dtype dt, const adakv_layer_shape& s, int64_t pool_kernel);
 bool score_window_tc_supported(adakv_dtype dt, const adakv_layer_shape& s, int64_t pool_kernel);
 size_t score_window_tc_workspace(const adakv_layer_shape& s);
 adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, int32_t scale,
                              const void* q, const void* k, void* head_scores, void* group_scores,
-                             void* ws, cudaStream_t stream);
+                             void* ws, uint32_t* err, cudaStream_t stream);
 
 
 adakv_status launch_layout(const int32_t* budgets, int64_t P, int64_t G, int64_t m, int64_t reserve,
                            int64_t layer_budget, const int64_t* layer_budgets, int32_t* seg_start,
-                           int32_t* seqlens, cudaStream_t stream);
+                           int32_t* seqlens, int32_t* seg_cap, cudaStream_t stream);
 adakv_status launch_gather(adakv_dtype dt, const adakv_layer_shape& s, int64_t max_rows,
                            const void* k, const void* v, const int32_t* budgets,
                            const int32_t* kept_pos, int64_t kept_stride, const int32_t* seg_start,
-                           void* k_cache, void* v_cache, cudaStream_t stream);
+                           void* k_cache, void* v_cache, uint32_t* err, cudaStream_t stream);
+adakv_status launch_validate(adakv_dtype dt, const void* data, int64_t n, uint32_t* err, cudaStream_t stream);
 size_t decode_workspace_bytes(int64_t P, int64_t H, int64_t G, int64_t d, int64_t max_rows, size_t acc);
 adakv_status launch_decode(adakv_dtype dt, int64_t P, int64_t H, int64_t G, int64_t d, int32_t scale,
-                           const void* q, void* kc, void* vc, int64_t cache_rows, const int32_t* ss, int32_t* sl,
-                           int64_t max_rows, const void* kn, const void* vn, void* out, void* ws,
-                           bool overlap_prev, cudaStream_t stream);
+                           const void* q, void* kc, void* vc, int64_t cache_rows, const int32_t* ss,
+                           const int32_t* cap, int32_t* sl, int64_t max_rows, const void* kn, const void* vn,
+                           void* out, void* ws, uint32_t* err, bool overlap_prev, cudaStream_t stream);
 adakv_status launch_append(adakv_dtype dt, int64_t segments, int64_t rows, int64_t d, void* kc, void* vc,
-                           const int32_t* ss, int32_t* sl, const void* kn, const void* vn,
-                           cudaStream_t stream);
+                           const int32_t* ss, const int32_t* cap, int32_t* sl, const void* kn, const void* vn,
+                           uint32_t* err, cudaStream_t stream);
 __global__ void budget_kernel(int op, const double* quotas_in, const int64_t* a_in, int64_t h,
                               int64_t total, double alpha, double bmax, double bmin,
                               const int64_t* caps_in, int64_t* out, double* quotas,
                               uint64_t* caps, uint64_t* tmp_a, uint64_t* tmp_o, uint32_t* err);
 
 // ---------------------------------------------------------------- launch ordering
-// The decode kernel reads its segments' rows and lengths before griddepcontrol.wait, so it
-// may overlap (programmatic dependent launch) only a predecessor that does not write them:
-// a decode of OTHER segments (the next layer of a model-wide plane).  Every entry point
-// that writes cache planes records itself here per stream; decode overlaps only when the
-// previous recorded launch on its stream was a decode on different segments.
+// The decode kernel reads its segments' rows, lengths and capacities before
+// griddepcontrol.wait, so it overlaps (programmatic dependent launch) its predecessor only
+// when the caller vouches, per call, that the predecessor writes none of them
+// (ADAKV_DECODE_CHAINED: a decode of other segments).  adakv_set_decode_overlap(0) turns
+// the overlap off globally (A/B measurements).
 namespace {
-std::mutex g_order_mu;
-struct LastLaunch {
-    cudaStream_t stream;
-    const void* decode_segments;  // nullptr: not a decode
-};
-std::vector<LastLaunch> g_last_launch;
 std::atomic<int> g_decode_overlap{-1};
 }  // namespace
-
-static const void* exchange_last_launch(cudaStream_t s, const void* decode_segments) {
-    std::lock_guard<std::mutex> lock(g_order_mu);
-    for (auto& e : g_last_launch)
-        if (e.stream == s) {
-            const void* prev = e.decode_segments;
-            e.decode_segments = decode_segments;
-            return prev;
-        }
-    if (g_last_launch.size() > 64) g_last_launch.erase(g_last_launch.begin());
-    g_last_launch.push_back({s, decode_segments});
-    return nullptr;
-}
 
 static bool decode_overlap_enabled() {
     int v = g_decode_overlap.load();
@@ -168,12 +150,12 @@ size_t score_ws(adakv_dtype dt, const adakv_layer_shape& s, int64_t pool_kernel)
 }
 
 adakv_status run_scores(adakv_dtype dt, const adakv_layer_shape& s, int64_t pool_kernel, int32_t scale,
-                        const void* q, const void* k, void* hs, void* gs, void* ws, cudaStream_t st) {
-    if (use_tc(dt, s, pool_kernel)) return score_window_tc(s, pool_kernel, scale, q, k, hs, gs, ws, st);
+                        const void* q, const void* k, void* hs, void* gs, void* ws, uint32_t* err, cudaStream_t st) {
+    if (use_tc(dt, s, pool_kernel)) return score_window_tc(s, pool_kernel, scale, q, k, hs, gs, ws, err, st);
     const size_t smem = score_window_generic_smem(dt, s, pool_kernel);
     if (smem > 227 * 1024)
         return fail(ADAKV_UNSUPPORTED, "window_scores: shape exceeds the generic kernel's shared memory");
-    return score_window_generic(dt, s, pool_kernel, scale, q, k, hs, gs, ws, st);
+    return score_window_generic(dt, s, pool_kernel, scale, q, k, hs, gs, ws, err, st);
 }
 
 struct CompressLayout {
@@ -201,10 +183,19 @@ CompressLayout compress_layout(void* base, adakv_dtype dt, const adakv_layer_sha
     return L;
 }
 
-__global__ void outside_totals_kernel(const int64_t* lb, int64_t P, int64_t bias, int64_t* out) {
-    for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += blockDim.x * gridDim.x)
-        out[i] = lb[i] - bias;
+// per-problem layer budgets outside the reference's floor / capacity (policies.hpp:229-231,
+// budget.hpp:48-59) latch ERR_BUDGET and become a zero outside total; select then rejects
+// the problem (zero budgets, nothing indexed)
+__global__ void outside_totals_kernel(const int64_t* lb, int64_t P, int64_t m, int64_t G, int64_t n_o, int64_t* out,
+                                      uint32_t* err) {
+    for (int64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += blockDim.x * gridDim.x) {
+        const int64_t b = lb[i];
+        const bool ok = b >= m * G + G && b - m * G <= G * n_o;
+        out[i] = ok ? b - m * G : -1;
+        if (!ok) atomicOr(err, ERR_BUDGET);
+    }
 }
+
 
 adakv_status run_budget_kernel(int op, const double* quotas, const int64_t* a, int64_t h,
                                int64_t total, double alpha, double bmax, double bmin,
@@ -276,7 +267,24 @@ adakv_status adakv_workspace_status(const void* workspace, adakv_stream_t stream
     if (e & ERR_REPAIR) return fail(ADAKV_INVALID_ARGUMENT, "evict_layer: cannot guarantee one element per head");
     if (e & ERR_BUDGET) return fail(ADAKV_INVALID_ARGUMENT, "topk_decision: k exceeds length");
     if (e & ERR_CAPACITY) return fail(ADAKV_INVALID_ARGUMENT, "append_kv: capacity exhausted");
+    if (e & ERR_MAXROWS) return fail(ADAKV_INVALID_ARGUMENT, "decode: segment longer than max_rows");
     return ADAKV_OK;
+}
+
+adakv_status adakv_clear_workspace_status(void* workspace, adakv_stream_t stream) {
+    if (!workspace) return fail(ADAKV_INVALID_ARGUMENT, "workspace: null");
+    ADAKV_CUDA_TRY(cudaMemsetAsync(workspace, 0, 4, reinterpret_cast<cudaStream_t>(stream)));
+    return ADAKV_OK;
+}
+
+adakv_status adakv_validate_finite(adakv_dtype dtype, const void* data, int64_t n, void* workspace,
+                                   adakv_stream_t stream) {
+    ADAKV_TRY(validate_dtype(dtype));
+    if (n < 0) return fail(ADAKV_INVALID_ARGUMENT, "validate: negative element count");
+    if (!workspace) return fail(ADAKV_INVALID_ARGUMENT, "validate: null workspace");
+    if (n == 0) return ADAKV_OK;
+    if (!data) return fail(ADAKV_INVALID_ARGUMENT, "validate: null data");
+    return launch_validate(dtype, data, n, static_cast<uint32_t*>(workspace), reinterpret_cast<cudaStream_t>(stream));
 }
 
 // ------------------------------------------------------------------ scoring
@@ -302,7 +310,8 @@ adakv_status adakv_window_scores(adakv_dtype dtype, const adakv_layer_shape* sha
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     ADAKV_CUDA_TRY(cudaMemsetAsync(workspace, 0, 4, st));
     void* ws = static_cast<char*>(workspace) + kWsHeader;
-    return run_scores(dtype, *shape, pool_kernel, scale, q, k, head_scores, group_scores, ws, st);
+    return run_scores(dtype, *shape, pool_kernel, scale, q, k, head_scores, group_scores, ws,
+                      static_cast<uint32_t*>(workspace), st);
 }
 
 // ------------------------------------------------------------------ selection
@@ -368,19 +377,19 @@ adakv_status adakv_segmented_select(adakv_dtype key_dtype, int64_t problems, int
 adakv_status adakv_gather(adakv_dtype dtype, const adakv_layer_shape* shape, int64_t layer_budget,
                           const int64_t* layer_budgets, const void* k, const void* v, const int32_t* budgets,
                           const int32_t* kept_pos, int64_t kept_stride, int64_t reserve, void* k_cache,
-                          void* v_cache, int32_t* seg_start, int32_t* seqlens, adakv_stream_t stream) {
+                          void* v_cache, int32_t* seg_start, int32_t* seqlens, int32_t* seg_cap, void* workspace,
+                          adakv_stream_t stream) {
     ADAKV_TRY(validate_dtype(dtype));
     ADAKV_TRY(validate_shape(shape));
     if (reserve < 0) return fail(ADAKV_INVALID_ARGUMENT, "gather: negative reserve");
     if (shape->problems == 0) return ADAKV_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    exchange_last_launch(st, nullptr);
     const int64_t G = shape->kv_groups, m = shape->window;
     ADAKV_TRY(launch_layout(budgets, shape->problems, G, m, reserve, layer_budget, layer_budgets, seg_start,
-                            seqlens, st));
+                            seqlens, seg_cap, st));
     const int64_t max_rows = layer_budgets ? G * (shape->outside + m) : layer_budget;
     return launch_gather(dtype, *shape, max_rows, k, v, budgets, kept_pos, kept_stride, seg_start, k_cache,
-                         v_cache, st);
+                         v_cache, static_cast<uint32_t*>(workspace), st);
 }
 
 // ------------------------------------------------------------------ compress
@@ -405,7 +414,8 @@ adakv_status adakv_compress_workspace(adakv_dtype dtype, const adakv_layer_shape
 adakv_status adakv_compress(adakv_dtype dtype, const adakv_layer_shape* shape, const adakv_policy_config* cfg,
                             int64_t layer_budget, const int64_t* layer_budgets, const void* q,
                             const void* k, const void* v, int64_t reserve, void* k_cache, void* v_cache,
-                            int32_t* seg_start, int32_t* seqlens, int32_t* budgets, void* group_scores,
+                            int32_t* seg_start, int32_t* seqlens, int32_t* seg_cap, int32_t* budgets,
+                            void* group_scores,
                             uint8_t* keep, void* workspace, size_t workspace_bytes, adakv_stream_t stream) {
     ADAKV_TRY(validate_dtype(dtype));
     ADAKV_TRY(validate_config(cfg));
@@ -429,13 +439,12 @@ adakv_status adakv_compress(adakv_dtype dtype, const adakv_layer_shape* shape, c
     if (workspace_bytes < L.bytes) return fail(ADAKV_WORKSPACE_TOO_SMALL, "compress: workspace too small");
     if (s.problems == 0) return ADAKV_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    exchange_last_launch(st, nullptr);
     ADAKV_CUDA_TRY(cudaMemsetAsync(workspace, 0, 4, st));
     void* scores = group_scores ? group_scores : L.scores;
 
     // K1: observation-window scores for every group (scoring runs for every kind,
     // policies.hpp:239-247)
-    ADAKV_TRY(run_scores(dtype, s, cfg->pool_kernel, cfg->scale, q, k, nullptr, scores, L.score_ws, st));
+    ADAKV_TRY(run_scores(dtype, s, cfg->pool_kernel, cfg->scale, q, k, nullptr, scores, L.score_ws, L.err, st));
 
     // K2/K3 selection
     SelParams prm{};
@@ -451,8 +460,8 @@ adakv_status adakv_compress(adakv_dtype dtype, const adakv_layer_shape* shape, c
     prm.sink = cfg->sink_tokens;
     prm.total = layer_budget - m * G;
     if (layer_budgets) {
-        outside_totals_kernel<<<unsigned(ceil_div(s.problems, 256)), 256, 0, st>>>(layer_budgets, s.problems,
-                                                                                m * G, L.totals);
+        outside_totals_kernel<<<unsigned(ceil_div(s.problems, 256)), 256, 0, st>>>(layer_budgets, s.problems, m,
+                                                                                G, n_o, L.totals, L.err);
         ADAKV_CUDA_TRY(cudaGetLastError());
         prm.totals = L.totals;
     }
@@ -466,10 +475,10 @@ adakv_status adakv_compress(adakv_dtype dtype, const adakv_layer_shape* shape, c
 
     // layout + K3 gather into the varlen planes
     ADAKV_TRY(launch_layout(budgets, s.problems, G, m, reserve, layer_budget, layer_budgets, seg_start,
-                            seqlens, st));
+                            seqlens, seg_cap, st));
     const int64_t max_rows = layer_budgets ? G * (n_o + m) : layer_budget;
     return launch_gather(dtype, s, max_rows, k, v, budgets, L.kept_pos, L.kept_stride, seg_start, k_cache,
-                         v_cache, st);
+                         v_cache, L.err, st);
 }
 
 // ------------------------------------------------------------------ decode
@@ -481,9 +490,9 @@ adakv_status adakv_decode_workspace(int64_t problems, int64_t q_heads, int64_t k
 
 adakv_status adakv_decode(adakv_dtype dtype, int64_t problems, int64_t q_heads, int64_t kv_groups,
                           int64_t head_dim, int32_t scale, const void* q, void* k_cache, void* v_cache,
-                          int64_t cache_rows, const int32_t* seg_start, int32_t* seqlens, int64_t max_rows, const void* k_new,
-                          const void* v_new, void* out, void* workspace, size_t workspace_bytes,
-                          adakv_stream_t stream) {
+                          int64_t cache_rows, const int32_t* seg_start, const int32_t* seg_cap, int32_t* seqlens,
+                          int64_t max_rows, const void* k_new, const void* v_new, void* out, void* workspace,
+                          size_t workspace_bytes, uint32_t flags, adakv_stream_t stream) {
     ADAKV_TRY(validate_dtype(dtype));
     if (kv_groups <= 0 || q_heads <= 0 || q_heads % kv_groups != 0)
         return fail(ADAKV_INVALID_ARGUMENT, "attention_output: head count mismatch");
@@ -492,16 +501,17 @@ adakv_status adakv_decode(adakv_dtype dtype, int64_t problems, int64_t q_heads, 
         return fail(ADAKV_INVALID_ARGUMENT, "append_kv: k and v must both be given");
     if (max_rows <= 0) return fail(ADAKV_INVALID_ARGUMENT, "attention_weights: empty key set");
     if (cache_rows <= 0) return fail(ADAKV_INVALID_ARGUMENT, "decode: empty cache plane");
+    if (!seg_start || !seqlens || !seg_cap) return fail(ADAKV_INVALID_ARGUMENT, "decode: null segment table");
+    if (flags & ~uint32_t(ADAKV_DECODE_CHAINED)) return fail(ADAKV_INVALID_ARGUMENT, "decode: unknown flags");
     const size_t need = kWsHeader + decode_workspace_bytes(problems, q_heads, kv_groups, head_dim, max_rows,
                                                            acc_size(dtype));
     if (workspace_bytes < need) return fail(ADAKV_WORKSPACE_TOO_SMALL, "decode: workspace too small");
     if (problems == 0) return ADAKV_OK;
     const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const void* prev = exchange_last_launch(st, seg_start);
-    const bool overlap = decode_overlap_enabled() && prev != nullptr && prev != seg_start;
+    const bool overlap = (flags & ADAKV_DECODE_CHAINED) && decode_overlap_enabled();
     return launch_decode(dtype, problems, q_heads, kv_groups, head_dim, scale, q, k_cache, v_cache, cache_rows,
-                         seg_start, seqlens, max_rows, k_new, v_new, out, static_cast<char*>(workspace) + kWsHeader,
-                         overlap, st);
+                         seg_start, seg_cap, seqlens, max_rows, k_new, v_new, out,
+                         static_cast<char*>(workspace) + kWsHeader, static_cast<uint32_t*>(workspace), overlap, st);
 }
 
 adakv_status adakv_host_device_pointer(const void* host, void** device_ptr) {
@@ -522,27 +532,26 @@ int adakv_set_decode_overlap(int enabled) {
     return prev;
 }
 
-adakv_status adakv_append_kv(adakv_dtype dtype, int64_t segments, int64_t head_dim, void* k_cache,
-                             void* v_cache, const int32_t* seg_start, int32_t* seqlens, const void* k_new,
-                             const void* v_new, adakv_stream_t stream) {
-    ADAKV_TRY(validate_dtype(dtype));
-    if (segments < 0) return fail(ADAKV_OUT_OF_RANGE, "append_kv: head index out of range");
-    exchange_last_launch(reinterpret_cast<cudaStream_t>(stream), nullptr);
-    return launch_append(dtype, segments, 1, head_dim, k_cache, v_cache, seg_start, seqlens, k_new, v_new,
-                         reinterpret_cast<cudaStream_t>(stream));
-}
-
 adakv_status adakv_append_rows(adakv_dtype dtype, int64_t segments, int64_t rows, int64_t head_dim,
-                               void* k_cache, void* v_cache, const int32_t* seg_start, int32_t* seqlens,
-                               const void* k_new, const void* v_new, adakv_stream_t stream) {
+                               void* k_cache, void* v_cache, const int32_t* seg_start, const int32_t* seg_cap,
+                               int32_t* seqlens, const void* k_new, const void* v_new, void* workspace,
+                               adakv_stream_t stream) {
     ADAKV_TRY(validate_dtype(dtype));
     if (segments < 0) return fail(ADAKV_OUT_OF_RANGE, "append_kv: head index out of range");
     if (rows < 0) return fail(ADAKV_INVALID_ARGUMENT, "append_kv: negative row count");
-    if ((k_new == nullptr || v_new == nullptr) && rows > 0 && segments > 0)
-        return fail(ADAKV_INVALID_ARGUMENT, "append_kv: k and v must both be given");
-    exchange_last_launch(reinterpret_cast<cudaStream_t>(stream), nullptr);
-    return launch_append(dtype, segments, rows, head_dim, k_cache, v_cache, seg_start, seqlens, k_new, v_new,
-                         reinterpret_cast<cudaStream_t>(stream));
+    if (segments == 0 || rows == 0) return ADAKV_OK;
+    if (k_new == nullptr || v_new == nullptr) return fail(ADAKV_INVALID_ARGUMENT, "append_kv: k and v must both be given");
+    if (!seg_start || !seg_cap || !seqlens) return fail(ADAKV_INVALID_ARGUMENT, "append_kv: null segment table");
+    if (!workspace) return fail(ADAKV_INVALID_ARGUMENT, "append_kv: null workspace");
+    return launch_append(dtype, segments, rows, head_dim, k_cache, v_cache, seg_start, seg_cap, seqlens, k_new,
+                         v_new, static_cast<uint32_t*>(workspace), reinterpret_cast<cudaStream_t>(stream));
+}
+
+adakv_status adakv_append_kv(adakv_dtype dtype, int64_t segments, int64_t head_dim, void* k_cache,
+                             void* v_cache, const int32_t* seg_start, const int32_t* seg_cap, int32_t* seqlens,
+                             const void* k_new, const void* v_new, void* workspace, adakv_stream_t stream) {
+    return adakv_append_rows(dtype, segments, 1, head_dim, k_cache, v_cache, seg_start, seg_cap, seqlens, k_new,
+                             v_new, workspace, stream);
 }
 
 // ------------------------------------------------------------------ budget helpers

@@ -35,6 +35,7 @@ enum : uint32_t {
     ERR_BUDGET = 1u << 1,      // topk_decision k > n (policies.hpp:83), apportion capacity
     ERR_REPAIR = 1u << 2,      // repair_zero_budgets (policies.hpp:190-191)
     ERR_CAPACITY = 1u << 3,    // decode append beyond reserved capacity
+    ERR_MAXROWS = 1u << 4,     // a decode segment longer than the call's max_rows bound
 };
 
 // ---------------------------------------------------------------- workspace

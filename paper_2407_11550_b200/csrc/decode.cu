@@ -30,17 +30,21 @@ constexpr int kMaxGroupHeads = 16;
 template <class T, class A, int J, int GH>
 __global__ void __launch_bounds__(kDecThreads)
 decode_kernel(const T* __restrict__ q, T* __restrict__ k_cache, T* __restrict__ v_cache,
-              const int32_t* __restrict__ seg_start, int32_t* __restrict__ seqlens,
-              const T* __restrict__ k_new, const T* __restrict__ v_new, T* __restrict__ out,
-              int64_t H, int64_t G, int64_t d, A inv_scale, int64_t chunk, A* __restrict__ part_ml,
-              A* __restrict__ part_o, uint32_t* __restrict__ tickets) {
+              const int32_t* __restrict__ seg_start, const int32_t* __restrict__ seg_cap,
+              int32_t* __restrict__ seqlens, const T* __restrict__ k_new, const T* __restrict__ v_new,
+              T* __restrict__ out, int64_t H, int64_t G, int64_t d, A inv_scale, int64_t chunk,
+              A* __restrict__ part_ml, A* __restrict__ part_o, uint32_t* __restrict__ tickets,
+              uint32_t* __restrict__ err) {
     const int64_t split = blockIdx.x, g = blockIdx.y, p = blockIdx.z;
     const int64_t nsplit = gridDim.x;
     const int64_t gs = H / G;
     const int64_t pg = p * G + g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t L_old = seqlens[pg];
-    const bool append = k_new != nullptr;
+    // append_kv into a full segment is refused (no write past its capacity); the step then
+    // attends the existing rows and the error is latched for adakv_workspace_status
+    const bool append = k_new != nullptr && L_old < seg_cap[pg];
+    if (k_new != nullptr && !append && split == 0 && threadIdx.x == 0) atomicOr(err, ERR_CAPACITY);
     const int64_t L = L_old + (append ? 1 : 0);
     const int64_t base = seg_start[pg];
     const T* kn = append ? k_new + pg * d : nullptr;
@@ -166,10 +170,15 @@ decode_kernel(const T* __restrict__ q, T* __restrict__ k_cache, T* __restrict__ 
 // append_kv (attention.hpp:126-134), `rows` rows per segment: block s appends
 // new[s, 0..rows) after the segment's current end and advances seqlens[s] by rows.
 __global__ void append_kernel(int64_t segments, int64_t rows, int64_t d, const int32_t* __restrict__ seg_start,
-                              int32_t* __restrict__ seqlens, const uint16_t* __restrict__ kn,
-                              const uint16_t* __restrict__ vn, uint16_t* __restrict__ kc,
-                              uint16_t* __restrict__ vc, int64_t esz_units) {
+                              const int32_t* __restrict__ seg_cap, int32_t* __restrict__ seqlens,
+                              const uint16_t* __restrict__ kn, const uint16_t* __restrict__ vn,
+                              uint16_t* __restrict__ kc, uint16_t* __restrict__ vc, int64_t esz_units,
+                              uint32_t* __restrict__ err) {
     const int64_t s = blockIdx.x;
+    if (int64_t(seqlens[s]) + rows > int64_t(seg_cap[s])) {  // capacity exhausted: refuse, latch
+        if (threadIdx.x == 0) atomicOr(err, ERR_CAPACITY);
+        return;
+    }
     const int64_t row0 = int64_t(seg_start[s]) + seqlens[s];
     const int64_t w = d * esz_units;  // row width in 16-bit units
     for (int64_t i = threadIdx.x; i < rows * w; i += blockDim.x) {
@@ -182,8 +191,8 @@ __global__ void append_kernel(int64_t segments, int64_t rows, int64_t d, const i
 
 template <class T, int J, int GH>
 adakv_status launch_t(int64_t P, int64_t H, int64_t G, int64_t d, int32_t scale, const void* q,
-                      void* kc, void* vc, const int32_t* ss, int32_t* sl, int64_t max_rows,
-                      const void* kn, const void* vn, void* out, void* ws, int64_t chunk,
+                      void* kc, void* vc, const int32_t* ss, const int32_t* cap, int32_t* sl, int64_t max_rows,
+                      const void* kn, const void* vn, void* out, void* ws, uint32_t* err, int64_t chunk,
                       int64_t nsplit, cudaStream_t stream) {
     using A = typename Acc<T>::type;
     Arena ar(ws);
@@ -196,9 +205,9 @@ adakv_status launch_t(int64_t P, int64_t H, int64_t G, int64_t d, int32_t scale,
     auto kfn = decode_kernel<T, A, J, GH>;
     ADAKV_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kfn<<<grid, kDecThreads, smem, stream>>>(
-        static_cast<const T*>(q), static_cast<T*>(kc), static_cast<T*>(vc), ss, sl,
+        static_cast<const T*>(q), static_cast<T*>(kc), static_cast<T*>(vc), ss, cap, sl,
         static_cast<const T*>(kn), static_cast<const T*>(vn), static_cast<T*>(out), H, G, d, inv,
-        chunk, part_ml, part_o, tickets);
+        chunk, part_ml, part_o, tickets, err);
     ADAKV_CUDA_TRY(cudaGetLastError());
     (void)max_rows;
     return ADAKV_OK;
@@ -231,24 +240,17 @@ size_t decode_workspace_bytes(int64_t P, int64_t H, int64_t G, int64_t d, int64_
 
 bool decode_tc_supported(adakv_dtype dt, int64_t H, int64_t G, int64_t d, int64_t cache_rows);
 adakv_status launch_decode_tc(int64_t P, int64_t H, int64_t G, int32_t scale, const void* q, void* kc, void* vc,
-                              int64_t cache_rows, const int32_t* ss, int32_t* sl, const void* kn, const void* vn,
-                              void* out, bool overlap_prev, cudaStream_t stream);
-
-bool decode_umma_enabled();
-bool decode_umma_supported(adakv_dtype dt, int64_t P, int64_t H, int64_t G, int64_t d, int64_t max_rows,
-                           int64_t cache_rows);
-adakv_status launch_decode_umma(int64_t P, int64_t H, int64_t G, int32_t scale, const void* q, void* kc, void* vc,
-                                int64_t cache_rows, const int32_t* ss, int32_t* sl, const void* kn, const void* vn,
-                                void* out, bool overlap_prev, cudaStream_t stream);
+                              int64_t cache_rows, const int32_t* ss, const int32_t* cap, int32_t* sl,
+                              const void* kn, const void* vn, void* out, uint32_t* err, bool overlap_prev,
+                              cudaStream_t stream);
 
 adakv_status launch_decode(adakv_dtype dt, int64_t P, int64_t H, int64_t G, int64_t d, int32_t scale,
-                           const void* q, void* kc, void* vc, int64_t cache_rows, const int32_t* ss, int32_t* sl,
-                           int64_t max_rows, const void* kn, const void* vn, void* out, void* ws,
-                           bool overlap_prev, cudaStream_t stream) {
-    if (decode_umma_enabled() && decode_umma_supported(dt, P, H, G, d, max_rows, cache_rows))
-        return launch_decode_umma(P, H, G, scale, q, kc, vc, cache_rows, ss, sl, kn, vn, out, overlap_prev, stream);
+                           const void* q, void* kc, void* vc, int64_t cache_rows, const int32_t* ss,
+                           const int32_t* cap, int32_t* sl, int64_t max_rows, const void* kn, const void* vn,
+                           void* out, void* ws, uint32_t* err, bool overlap_prev, cudaStream_t stream) {
     if (decode_tc_supported(dt, H, G, d, cache_rows))
-        return launch_decode_tc(P, H, G, scale, q, kc, vc, cache_rows, ss, sl, kn, vn, out, overlap_prev, stream);
+        return launch_decode_tc(P, H, G, scale, q, kc, vc, cache_rows, ss, cap, sl, kn, vn, out, err, overlap_prev,
+                                stream);
     int64_t chunk, nsplit;
     decode_plan(P, G, max_rows, &chunk, &nsplit);
     if (H / G > kMaxGroupHeads) return fail(ADAKV_UNSUPPORTED, "decode: more than 16 query heads per KV group");
@@ -259,11 +261,11 @@ adakv_status launch_decode(adakv_dtype dt, int64_t P, int64_t H, int64_t G, int6
     const int Js = J <= 1 ? 1 : J <= 2 ? 2 : J <= 4 ? 4 : 8;
 #define ADAKV_DEC_GH(T, JJ)                                                                     \
     switch (GHs) {                                                                              \
-        case 1: return launch_t<T, JJ, 1>(P, H, G, d, scale, q, kc, vc, ss, sl, max_rows, kn, vn, out, ws, chunk, nsplit, stream); \
-        case 2: return launch_t<T, JJ, 2>(P, H, G, d, scale, q, kc, vc, ss, sl, max_rows, kn, vn, out, ws, chunk, nsplit, stream); \
-        case 4: return launch_t<T, JJ, 4>(P, H, G, d, scale, q, kc, vc, ss, sl, max_rows, kn, vn, out, ws, chunk, nsplit, stream); \
-        case 8: return launch_t<T, JJ, 8>(P, H, G, d, scale, q, kc, vc, ss, sl, max_rows, kn, vn, out, ws, chunk, nsplit, stream); \
-        default: return launch_t<T, JJ, 16>(P, H, G, d, scale, q, kc, vc, ss, sl, max_rows, kn, vn, out, ws, chunk, nsplit, stream); \
+        case 1: return launch_t<T, JJ, 1>(P, H, G, d, scale, q, kc, vc, ss, cap, sl, max_rows, kn, vn, out, ws, err, chunk, nsplit, stream); \
+        case 2: return launch_t<T, JJ, 2>(P, H, G, d, scale, q, kc, vc, ss, cap, sl, max_rows, kn, vn, out, ws, err, chunk, nsplit, stream); \
+        case 4: return launch_t<T, JJ, 4>(P, H, G, d, scale, q, kc, vc, ss, cap, sl, max_rows, kn, vn, out, ws, err, chunk, nsplit, stream); \
+        case 8: return launch_t<T, JJ, 8>(P, H, G, d, scale, q, kc, vc, ss, cap, sl, max_rows, kn, vn, out, ws, err, chunk, nsplit, stream); \
+        default: return launch_t<T, JJ, 16>(P, H, G, d, scale, q, kc, vc, ss, cap, sl, max_rows, kn, vn, out, ws, err, chunk, nsplit, stream); \
     }
 #define ADAKV_DEC_SWITCH(T)                 \
     switch (Js) {                           \
@@ -283,13 +285,13 @@ adakv_status launch_decode(adakv_dtype dt, int64_t P, int64_t H, int64_t G, int6
 }
 
 adakv_status launch_append(adakv_dtype dt, int64_t segments, int64_t rows, int64_t d, void* kc, void* vc,
-                           const int32_t* ss, int32_t* sl, const void* kn, const void* vn,
-                           cudaStream_t stream) {
+                           const int32_t* ss, const int32_t* cap, int32_t* sl, const void* kn, const void* vn,
+                           uint32_t* err, cudaStream_t stream) {
     if (segments == 0 || rows == 0) return ADAKV_OK;
     const int64_t units = int64_t(dtype_size(dt)) / 2;
     append_kernel<<<unsigned(segments), 128, 0, stream>>>(
-        segments, rows, d, ss, sl, static_cast<const uint16_t*>(kn), static_cast<const uint16_t*>(vn),
-        static_cast<uint16_t*>(kc), static_cast<uint16_t*>(vc), units);
+        segments, rows, d, ss, cap, sl, static_cast<const uint16_t*>(kn), static_cast<const uint16_t*>(vn),
+        static_cast<uint16_t*>(kc), static_cast<uint16_t*>(vc), units, err);
     ADAKV_CUDA_TRY(cudaGetLastError());
     return ADAKV_OK;
 }

@@ -165,9 +165,10 @@ __global__ void __launch_bounds__(32 * W, 1)
 decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                  const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ k_cache,
                  __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ seg_start,
-                 int32_t* __restrict__ seqlens, const __nv_bfloat16* __restrict__ k_new,
-                 const __nv_bfloat16* __restrict__ v_new, __nv_bfloat16* __restrict__ out, int H, int G,
-                 float scale_log2, int nslots, int qmode, unsigned long long* __restrict__ dbg) {
+                 const int32_t* __restrict__ seg_cap, int32_t* __restrict__ seqlens,
+                 const __nv_bfloat16* __restrict__ k_new, const __nv_bfloat16* __restrict__ v_new,
+                 __nv_bfloat16* __restrict__ out, uint32_t* __restrict__ err, int H, int G, float scale_log2,
+                 int nslots, int qmode, unsigned long long* __restrict__ dbg) {
     constexpr int d = 128;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment by offsetting the __shared__ array itself (keeps the shared window,
@@ -182,7 +183,6 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     const int gs = H / G;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
-    const bool append = k_new != nullptr;
     const bool head_ok = gid < gs;
     uint8_t* ring = ring_of(warp);  // this warp's TMA slots
     auto stamp = [&](int k) {       // (debug) per-CTA phase timestamps
@@ -196,6 +196,9 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     // this layer's own cache state (written by its previous decode step, long complete)
     const int L_old = __ldcg(seqlens + pg);
     const int base = seg_start[pg];
+    // append_kv into a full segment is refused (never written past seg_cap): the step attends
+    // the existing rows and ERR_CAPACITY is latched after the dependency wait
+    const bool append = k_new != nullptr && L_old < seg_cap[pg];
     stamp(0);
     // rank r finishes output columns [128 r / CS, 128 (r+1) / CS) of every head
     constexpr int chunk = chunk_floats(CS);
@@ -206,7 +209,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         mbar_fence_init();
         const int nq = (gs + 3) >> 2;  // head quads: each (column, quad) arrives as one 16-byte store
         mbar_arrive_expect_tx(&S.rbar, uint32_t(CS * nq * (32 + 16 * ncols)));
-        if (qmode == 1 || qmode == 2) {
+        if (qmode >= 1) {
             // query staging barrier: the group's gs rows land by one bulk copy (the cluster
             // barrier below orders this init before any multicast from rank 0)
             mbar_init(&S.qbar, 1);
@@ -272,6 +275,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (k_new != nullptr && !append && rank == 0 && threadIdx.x == 0) atomicOr(err, ERR_CAPACITY);
     stamp(2);
     // Q staging: mode 0 -- every lane loads its fragments from global memory (72 warps per
     // group hit the same 1 KB); mode 1 -- one bulk copy per CTA into shared memory; mode 2 --
@@ -352,7 +356,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     // zdep is always 0 but depends on the fetched fragments, which pins the assembly below
     // after fetch_k(0) (otherwise the compiler hoists it, and with it the wait for Q)
     const uint32_t zdep = (kva[0][0].x == 0x7fc00001u && nslots == -12345) ? 1u : 0u;
-    if (qmode == 1 || qmode == 2) {
+    if (qmode >= 1) {
         // every warp waits (also those without blocks: no multicast may land in an exited CTA)
         mbar_wait(&S.qbar, 0);
         const uint32_t qrow = smem_u32(S.qs) + uint32_t((head_ok ? gid : 0) * d * 2);
@@ -742,8 +746,9 @@ size_t decode_tc_workspace(int64_t, int64_t, int64_t, int64_t) { return 256; }
 extern "C" int adakv_debug_decode_cluster(int64_t P, int64_t G) { return int(decode_tc_cluster(P, G)); }
 
 adakv_status launch_decode_tc(int64_t P, int64_t H, int64_t G, int32_t scale, const void* q, void* kc, void* vc,
-                              int64_t cache_rows, const int32_t* ss, int32_t* sl, const void* kn, const void* vn,
-                              void* out, bool overlap_prev, cudaStream_t stream) {
+                              int64_t cache_rows, const int32_t* ss, const int32_t* cap, int32_t* sl,
+                              const void* kn, const void* vn, void* out, uint32_t* err, bool overlap_prev,
+                              cudaStream_t stream) {
     ADAKV_TRY(prepare_kernel());
     // tensor maps of the two planes (one pair serves every layer of a model-wide plane)
     static std::mutex mu;
@@ -787,9 +792,9 @@ adakv_status launch_decode_tc(int64_t P, int64_t H, int64_t G, int32_t scale, co
     cfg.attrs = attr;
     cfg.numAttrs = overlap_prev ? 2 : 1;
     ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel_for(cs), tk, tv, static_cast<const __nv_bfloat16*>(q),
-                                      static_cast<__nv_bfloat16*>(kc), static_cast<__nv_bfloat16*>(vc), ss, sl,
+                                      static_cast<__nv_bfloat16*>(kc), static_cast<__nv_bfloat16*>(vc), ss, cap, sl,
                                       static_cast<const __nv_bfloat16*>(kn), static_cast<const __nv_bfloat16*>(vn),
-                                      static_cast<__nv_bfloat16*>(out), int(H), int(G), sc, nslots, cs > 1 ? qmode : (qmode ? 1 : 0), dbg_buf()));
+                                      static_cast<__nv_bfloat16*>(out), err, int(H), int(G), sc, nslots, cs > 1 ? qmode : (qmode ? 1 : 0), dbg_buf()));
     return ADAKV_OK;
 }
 

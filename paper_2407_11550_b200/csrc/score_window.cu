@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kThreads)
 scores_kernel(const T* __restrict__ q, const T* __restrict__ k, int64_t H, int64_t G, int64_t m,
               int64_t n_o, int64_t n_rows, int64_t d, A inv_scale, int pad,
               const A* __restrict__ stats, int64_t nchunks, A* __restrict__ head_scores,
-              A* __restrict__ group_scores) {
+              A* __restrict__ group_scores, uint32_t* __restrict__ err) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int64_t pg = blockIdx.y;
     const int64_t p = pg / G, g = pg % G;
@@ -146,6 +146,10 @@ scores_kernel(const T* __restrict__ q, const T* __restrict__ k, int64_t H, int64
             if (st[2 * c] != neg_inf<A>()) S += st[2 * c + 1] * acc_exp(st[2 * c] - M);
         rowM[r] = M;
         rowS[r] = S;
+        // a NaN or +Inf logit anywhere in the row (a non-finite key, LayerCache::validate,
+        // attention.hpp:76-83) leaves a non-finite maximum or sum
+        if (blockIdx.x == 0 && err && !(M > neg_inf<A>() && M < A(INFINITY) && S >= A(1) && S < A(INFINITY)))
+            atomicOr(err, ERR_NONFINITE);
     }
     for (int64_t i = tid; i < gs * kChunk; i += kThreads) acc[i] = A(0);
 
@@ -221,7 +225,7 @@ scores_kernel(const T* __restrict__ q, const T* __restrict__ k, int64_t H, int64
 template <class T>
 adakv_status launch_generic(const adakv_layer_shape& s, int64_t pool_kernel, int32_t scale,
                             const void* q, const void* k, void* head_scores, void* group_scores,
-                            void* ws, cudaStream_t stream) {
+                            void* ws, uint32_t* err, cudaStream_t stream) {
     using A = typename Acc<T>::type;
     const int64_t P = s.problems, H = s.q_heads, G = s.kv_groups, m = s.window, n_o = s.outside,
                   d = s.head_dim;
@@ -245,7 +249,7 @@ adakv_status launch_generic(const adakv_layer_shape& s, int64_t pool_kernel, int
     ADAKV_CUDA_TRY(cudaGetLastError());
     k2<<<grid, kThreads, smem2, stream>>>(static_cast<const T*>(q), static_cast<const T*>(k), H, G, m,
                                          n_o, n_o + m, d, inv, pad, stats, nchunks,
-                                         static_cast<A*>(head_scores), static_cast<A*>(group_scores));
+                                         static_cast<A*>(head_scores), static_cast<A*>(group_scores), err);
     ADAKV_CUDA_TRY(cudaGetLastError());
     return ADAKV_OK;
 }
@@ -269,11 +273,11 @@ size_t score_window_generic_smem(adakv_dtype dt, const adakv_layer_shape& s, int
 
 adakv_status score_window_generic(adakv_dtype dt, const adakv_layer_shape& s, int64_t pool_kernel,
                                   int32_t scale, const void* q, const void* k, void* head_scores,
-                                  void* group_scores, void* ws, cudaStream_t stream) {
+                                  void* group_scores, void* ws, uint32_t* err, cudaStream_t stream) {
     switch (dt) {
-        case ADAKV_F64: return launch_generic<double>(s, pool_kernel, scale, q, k, head_scores, group_scores, ws, stream);
-        case ADAKV_F32: return launch_generic<float>(s, pool_kernel, scale, q, k, head_scores, group_scores, ws, stream);
-        case ADAKV_BF16: return launch_generic<__nv_bfloat16>(s, pool_kernel, scale, q, k, head_scores, group_scores, ws, stream);
+        case ADAKV_F64: return launch_generic<double>(s, pool_kernel, scale, q, k, head_scores, group_scores, ws, err, stream);
+        case ADAKV_F32: return launch_generic<float>(s, pool_kernel, scale, q, k, head_scores, group_scores, ws, err, stream);
+        case ADAKV_BF16: return launch_generic<__nv_bfloat16>(s, pool_kernel, scale, q, k, head_scores, group_scores, ws, err, stream);
     }
     return fail(ADAKV_INVALID_ARGUMENT, "window_scores: unknown dtype");
 }

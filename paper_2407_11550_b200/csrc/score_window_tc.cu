@@ -89,6 +89,7 @@ struct TcParams {
     float* head_scores;  // [P][H][n_o] or null
     float* group_scores; // [P][G][n_o]
     long long* dbg;      // (debug) per-CTA role wait counters, 16 per CTA per pass, or null
+    uint32_t* err;       // error word (ERR_NONFINITE) or null
 };
 
 // ------------------------------------------------------------------ epilogue helpers
@@ -531,6 +532,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                             if (mc != -INFINITY) Sf += red[(c * 128 + r) * 2 + 1] * ex2(mc - Mf);
                         }
                         float* fs = prm.final_stats + (size_t(gpg) * 128 + r) * 2;
+                        // a NaN or +Inf logit anywhere in the row (a non-finite key,
+                        // LayerCache::validate, attention.hpp:76-83) leaves a non-finite max or sum
+                        if (active && prm.err && !(Mf > -INFINITY && Mf < INFINITY && Sf >= 1.f && Sf < INFINITY))
+                            atomicOr(prm.err, ERR_NONFINITE);
                         fs[0] = Mf;
                         fs[1] = active ? Mf + __log2f(Sf) + prm.log2_m : INFINITY;
                         if (et == 0) prm.tickets[pg] = 0u;
@@ -624,7 +629,8 @@ size_t score_window_tc_workspace(const adakv_layer_shape& s) {
 }
 
 adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, int32_t scale, const void* q,
-                             const void* k, void* head_scores, void* group_scores, void* ws, cudaStream_t stream) {
+                             const void* k, void* head_scores, void* group_scores, void* ws, uint32_t* err,
+                             cudaStream_t stream) {
     const int pad = int((pool_kernel - 1) / 2);
     const Plan pl = make_plan(s, pad);
     const int64_t G = s.kv_groups, H = s.q_heads, gs = H / G, m = s.window, n = s.outside + s.window;
@@ -669,6 +675,7 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
         }();
         prm.debug = dbg;
         prm.dbg = g_score_dbg;
+        prm.err = err;
         // pass 1: row statistics over 128-key tiles
         prm.pass = 1;
         prm.step = kTile;

@@ -152,11 +152,19 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     __shared__ unsigned char seg_r0[kMaxSeg], seg_r1[kMaxSeg];
     __shared__ int c_s0, c_s1;
     for (int s = tid; s <= S; s += kSelThreads) s_off[s] = prm.off[s];
+    // rank owning flat element e: the exact inverse of the slice split above (CTA t owns
+    // [N t / CS, N (t+1) / CS)), i.e. the largest t with floor(N t / CS) <= e
+    auto rank_of = [&](int64_t e) -> unsigned {
+        unsigned r = 0;
+        for (unsigned t = 1; t < CS; ++t)
+            if (N * int64_t(t) / int64_t(CS) <= e) r = t;
+        return r;
+    };
     for (int s = tid; s < S; s += kSelThreads) {
         seg_gt[s] = 0;
         b_caps[s] = uint64_t(prm.off[s + 1] - prm.off[s]);
-        seg_r0[s] = (unsigned char)((prm.off[s] * CS) / N);
-        seg_r1[s] = (unsigned char)(((prm.off[s + 1] > 0 ? prm.off[s + 1] - 1 : 0) * CS) / N);
+        seg_r0[s] = (unsigned char)rank_of(prm.off[s]);
+        seg_r1[s] = (unsigned char)rank_of(prm.off[s + 1] > 0 ? prm.off[s + 1] - 1 : 0);
     }
 
     // Every pass below re-reads this CTA's slice of keys: read the scores from global memory
@@ -331,7 +339,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
 
     // ---------------- Phase A: layer-wide top-k (Algorithm 1, budget.hpp:118-140)
     const bool adaptive = prm.alloc_mode == ADAKV_ALLOC_ADAPTIVE;
-    if (adaptive && g_k > 0) {
+    if (adaptive && g_k > 0 && g_k <= N) {
         __shared__ int64_t g_krem;
         __shared__ KT g_prefix;
         if (tid == 0) {
@@ -397,8 +405,13 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     // ---------------- Phase C: allocation (one thread, redundantly per CTA, bit-exact fp64)
     if (tid == 0) {
         uint32_t e = 0;
-        const uint64_t k = uint64_t(g_k);
-        if (adaptive) {
+        // a per-problem total outside [0, N] (layer budget below the window floor or above the
+        // capacity, policies.hpp:229-231, budget.hpp:48-59) is rejected, never selected from
+        if (prm.alloc_mode != ADAKV_ALLOC_GIVEN && (g_k < 0 || g_k > N)) e |= ERR_BUDGET;
+        const uint64_t k = e ? 0 : uint64_t(g_k);
+        for (int s = 0; s < S; ++s) b_fin[s] = 0;
+        if (e) {
+        } else if (adaptive) {
             if (prm.blend) e |= safeguard_dev(b_raw, k, S, prm.alpha, b_caps, quotas, b_fin);
             else
                 for (int s = 0; s < S; ++s) b_fin[s] = b_raw[s];
@@ -412,6 +425,10 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
             }
         }
         if (!e && prm.repair) e |= repair_dev(b_fin, b_caps, S);
+        // on any error every budget is zero: the layout and gather after this kernel then copy
+        // the window rows only and never index kept positions that were not written
+        if (e)
+            for (int s = 0; s < S; ++s) b_fin[s] = 0;
         any_active = 0;
         for (int s = 0; s < S; ++s) {
             const int64_t b = int64_t(b_fin[s]), n = int64_t(b_caps[s]);
@@ -426,7 +443,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                 seg_mode[s] = MODE_NONE;
             } else if (b == n) {
                 seg_mode[s] = MODE_ALL;
-            } else if (adaptive && g_k > 0 && b_fin[s] == b_raw[s]) {
+            } else if (adaptive && g_k > 0 && g_k <= N && b_fin[s] == b_raw[s]) {
                 // per-segment top-b == the layer-wide selection restricted to s
                 seg_mode[s] = MODE_THRESH;
                 seg_T[s] = g_T;

@@ -45,8 +45,10 @@ _ws_cache: dict = {}
 
 
 def workspace(nbytes: int, device, key="default") -> torch.Tensor:
-    """Cached uint8 workspace (zero-initialised on first allocation)."""
-    k = (str(device), key)
+    """Cached uint8 workspace (zero-initialised on first allocation), one per (device, stream,
+    purpose): calls issued on different streams never share scratch.  A workspace returned by
+    an op is valid until the next op of the same purpose on the same stream."""
+    k = (str(device), torch.cuda.current_stream(device).cuda_stream, key)
     t = _ws_cache.get(k)
     if t is None or t.numel() < nbytes:
         t = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
@@ -71,7 +73,8 @@ class CompressedCache:
 
     Segment (p, g) holds rows [seg_start, seg_start + seqlens) of k/v: kept outside
     rows in original order, then the m window rows (policies.hpp:273-290);
-    capacity per segment = budgets + m + reserve.
+    capacity per segment = budgets + m + reserve (seg_cap); decode and append never write
+    past it (ERR_CAPACITY, raised by workspace_status).
     """
     k: torch.Tensor
     v: torch.Tensor
@@ -87,10 +90,28 @@ class CompressedCache:
     layer_budget: int
     scores: torch.Tensor | None = None  # [P, G, n_o] pooled group scores
     keep: torch.Tensor | None = None    # uint8 [P, G, n_o] decision
+    seg_cap: torch.Tensor | None = None  # int32 [P*G] capacity in rows (derived if not given)
+
+    def __post_init__(self):
+        if self.seg_cap is None:
+            # a hand-built cache of back-to-back segments: each runs to the next one's start
+            # (the last to the end of the planes)
+            st = self.seg_start.to(torch.int64)
+            if st.numel():
+                order = torch.argsort(st)
+                ends = torch.empty_like(st)
+                ends[order] = torch.cat([st[order][1:], st.new_tensor([self.k.shape[0]])])
+                self.seg_cap = (ends - st).to(torch.int32)
+            else:
+                self.seg_cap = self.seg_start.clone()
 
     @property
     def max_rows(self) -> int:
-        return self.layer_budget + self.reserve  # any segment fits in budget_total + reserve
+        """Upper bound of any segment's length: its largest capacity (seqlens <= seg_cap always).
+        Read from the device once (one synchronisation) and cached."""
+        if getattr(self, "_max_rows", None) is None:
+            self._max_rows = int(self.seg_cap.max()) if self.seg_cap.numel() else 1
+        return self._max_rows
 
     def segment(self, p: int, g: int):
         s = int(self.seg_start[p * self.G + g])
@@ -112,7 +133,7 @@ def host_device_pointer(t: torch.Tensor) -> C.c_void_p:
 def compress(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layer_budget: int, kind="ada_snapkv",
              pool_kernel=7, alpha=0.2, sink_tokens=4, scale=True, reserve=0, layer_budgets=None,
              return_scores=False, return_keep=False, out: CompressedCache | None = None,
-             ws: torch.Tensor | None = None, first_problem: int = 0) -> CompressedCache:
+             ws: torch.Tensor | None = None, first_problem: int = 0, validate=False, check=False) -> CompressedCache:
     """evict_layer (policies.hpp:204-293) for P problems at once.
 
     q [P, H, m, d]; k, v [P, G, n, d] with the observation window in the last m rows.
@@ -123,6 +144,11 @@ def compress(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layer_budget: in
     first_problem: with `out` and uniform budgets, write these P problems as problems
     [first_problem, first_problem + P) of `out` (a model's layers compressed in chunks, e.g. as
     their inputs arrive); the rows land exactly where one call over all problems puts them.
+    validate: also scan every K and V entry for NaN/Inf (LayerCache::validate,
+    attention.hpp:76-83; adakv_validate_finite).  Without it the device still latches the
+    non-finite entries that reach the window statistics or the copied rows.
+    check: synchronise and raise the reference's exception for anything the device latched
+    (non-finite input, per-problem budget below the floor / above the capacity).
     """
     _need_cuda(q, k)
     if v.is_cuda:
@@ -141,6 +167,12 @@ def compress(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layer_budget: in
     lib = L.lib()
     if layer_budgets is not None:
         lb_host = layer_budgets.detach().cpu().numpy().astype(np.int64)
+        # evict_layer's floor and apportion's capacity per problem (policies.hpp:229-231,
+        # budget.hpp:48-59); the device latches the same errors for direct C-ABI callers
+        if lb_host.size and int(lb_host.min()) < m * G + G:
+            raise L.InvalidArgument(1, "evict_layer: budget below the window-plus-one floor")
+        if lb_host.size and int(lb_host.max()) - m * G > G * n_o:
+            raise L.InvalidArgument(1, "apportion: total exceeds capacity")
         rows = int(lb_host.sum()) + P * G * reserve
         lbmax = int(lb_host.max()) if lb_host.size else 0
     else:
@@ -154,6 +186,7 @@ def compress(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layer_budget: in
             v=torch.empty((max(rows, 1), d), dtype=q.dtype, device=dev),
             seg_start=torch.empty(P * G, dtype=torch.int32, device=dev),
             seqlens=torch.empty(P * G, dtype=torch.int32, device=dev),
+            seg_cap=torch.empty(P * G, dtype=torch.int32, device=dev),
             budgets=torch.empty(P * G, dtype=torch.int32, device=dev),
             P=P, H=H, G=G, m=m, d=d, reserve=reserve, layer_budget=lbmax,
             scores=torch.empty((P, G, n_o), dtype=acc_dtype, device=dev) if return_scores else None,
@@ -174,12 +207,25 @@ def compress(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layer_budget: in
         ws = workspace(nbytes.value, dev, "compress")
     L.check(lib.adakv_compress(dt, C.byref(shape), C.byref(cfg), int(layer_budget), _p(layer_budgets), _p(q),
                                _p(k), v_ptr, int(reserve), at(out.k, row0 * d), at(out.v, row0 * d),
-                               at(out.seg_start, p0 * G), at(out.seqlens, p0 * G), at(out.budgets, p0 * G),
-                               at(out.scores, p0 * G * n_o), at(out.keep, p0 * G * n_o), _p(ws),
-                               ws.numel(), _stream()))
+                               at(out.seg_start, p0 * G), at(out.seqlens, p0 * G), at(out.seg_cap, p0 * G),
+                               at(out.budgets, p0 * G), at(out.scores, p0 * G * n_o), at(out.keep, p0 * G * n_o),
+                               _p(ws), ws.numel(), _stream()))
     if row0:  # the library laid the segments out from row 0 of the planes it was given
         out.seg_start[p0 * G:(p0 + P) * G] += row0
+    out._max_rows = None  # capacities were rewritten
+    if validate:
+        validate_finite(k, ws)
+        validate_finite(v, ws)
+    if check:
+        workspace_status(ws)
     return out
+
+
+def validate_finite(x: torch.Tensor, ws: torch.Tensor) -> None:
+    """LayerCache::validate (attention.hpp:76-83) on the device: latches a non-finite entry of x
+    (device or pinned host tensor) into ws's error word (raised by workspace_status)."""
+    ptr = _p(x) if x.is_cuda else host_device_pointer(x)
+    L.check(L.lib().adakv_validate_finite(_dt(x), ptr, x.numel(), _p(ws), _stream()))
 
 
 def window_scores(q: torch.Tensor, k: torch.Tensor, pool_kernel=7, scale=True, head_scores=False,
@@ -261,45 +307,57 @@ def decode_workspace_bytes(P, H, G, d, max_rows) -> int:
 
 def decode(q: torch.Tensor, cache: CompressedCache, k_new: torch.Tensor | None = None,
            v_new: torch.Tensor | None = None, scale=True, max_rows: int | None = None,
-           out: torch.Tensor | None = None, ws: torch.Tensor | None = None) -> torch.Tensor:
+           out: torch.Tensor | None = None, ws: torch.Tensor | None = None, check=False) -> torch.Tensor:
     """One decode step over the compressed cache (attention.hpp:169-196, report.hpp:133-144),
     with append_kv (attention.hpp:126-134) of (k_new, v_new) [P, G, d] fused in.
 
     q [P, H, d] -> out [P, H, d].  `ws` must be zero-initialised before first use
     (the kernel keeps its tickets re-armed), e.g. torch.zeros(decode_workspace_bytes(...)).
+    A segment already at capacity is not appended to; check=True synchronises and raises
+    append_kv's InvalidArgument for it (otherwise read it later with workspace_status(ws)).
     """
     _need_cuda(q, k_new, v_new)
     P, H, d = q.shape
-    mr = int(max_rows if max_rows is not None else cache.max_rows + 1)
+    mr = int(max_rows if max_rows is not None else cache.max_rows)
     if out is None:
         out = torch.empty_like(q)
     lib = L.lib()
     if ws is None:
         ws = workspace(decode_workspace_bytes(P, H, cache.G, d, mr), q.device, "decode")
     L.check(lib.adakv_decode(_dt(q), P, H, cache.G, d, int(bool(scale)), _p(q), _p(cache.k), _p(cache.v),
-                             cache.k.shape[0],
-                             _p(cache.seg_start), _p(cache.seqlens), mr, _p(k_new), _p(v_new), _p(out), _p(ws),
-                             ws.numel(), _stream()))
+                             cache.k.shape[0], _p(cache.seg_start), _p(cache.seg_cap), _p(cache.seqlens), mr,
+                             _p(k_new), _p(v_new), _p(out), _p(ws), ws.numel(), 0, _stream()))
+    if check:
+        workspace_status(ws)
     return out
 
 
-def append_kv(cache: CompressedCache, k_new: torch.Tensor, v_new: torch.Tensor) -> None:
-    """append_kv (attention.hpp:126-134) for every segment: k_new/v_new [P*G, d]."""
-    _need_cuda(k_new, v_new)
-    L.check(L.lib().adakv_append_kv(_dt(k_new), cache.P * cache.G, cache.d, _p(cache.k), _p(cache.v),
-                                    _p(cache.seg_start), _p(cache.seqlens), _p(k_new), _p(v_new), _stream()))
+def append_kv(cache: CompressedCache, k_new: torch.Tensor, v_new: torch.Tensor, check=True) -> None:
+    """append_kv (attention.hpp:126-134) for every segment: k_new/v_new [P*G, d].  A segment at
+    capacity is left untouched and (check=True) InvalidArgument is raised, as the reference
+    throws on a bad append (attention.hpp:128-131)."""
+    append_rows(cache, k_new.contiguous().reshape(k_new.shape[0], 1, -1),
+                v_new.contiguous().reshape(v_new.shape[0], 1, -1), check=check)
 
 
-def append_rows(cache: CompressedCache, k_new: torch.Tensor, v_new: torch.Tensor) -> None:
+def append_rows(cache: CompressedCache, k_new: torch.Tensor, v_new: torch.Tensor, check=True) -> None:
     """append_kv (attention.hpp:126-134) of T rows per segment: k_new/v_new [P*G, T, d] (e.g. the
     question tokens after a question-agnostic compression).  The cache needs T spare rows per
-    segment (compress(..., reserve >= T + decode steps))."""
+    segment (compress(..., reserve >= T + decode steps)); segments without them are left
+    untouched and (check=True) InvalidArgument("append_kv: capacity exhausted") is raised."""
+    k_new, v_new = k_new.contiguous(), v_new.contiguous()
     _need_cuda(k_new, v_new)
     S, T, d = k_new.shape
     if S != cache.P * cache.G or d != cache.d or v_new.shape != k_new.shape:
         raise L.InvalidArgument(1, "append_kv: row shape mismatch")
+    ws = workspace(256, k_new.device, "append")
+    if check:
+        L.check(L.lib().adakv_clear_workspace_status(_p(ws), _stream()))
     L.check(L.lib().adakv_append_rows(_dt(k_new), S, T, d, _p(cache.k), _p(cache.v), _p(cache.seg_start),
-                                      _p(cache.seqlens), _p(k_new.contiguous()), _p(v_new.contiguous()), _stream()))
+                                      _p(cache.seg_cap), _p(cache.seqlens), _p(k_new.contiguous()),
+                                      _p(v_new.contiguous()), _p(ws), _stream()))
+    if check:
+        workspace_status(ws)
 
 
 # ---------------------------------------------------------------- budget helpers (device fp64)

@@ -60,6 +60,21 @@ def compress_question_agnostic(q_ctx, k_ctx, v_ctx, layer_budget, k_question, v_
     return cache
 
 
+def decode_layer(lib, c, layer, batch, q, k_new, v_new, out, ws, max_rows, stream, chained, scale=1):
+    """adakv_decode of one layer's B*G segments of a model-wide cache (problems layer-major).
+    chained: the kernel enqueued just before on `stream` is the decode of another layer
+    (ADAKV_DECODE_CHAINED: its cache rows stream in while that one finishes)."""
+    G, H, d = c.G, c.H, c.d
+    seg = layer * batch * G
+    L.check(lib.adakv_decode(
+        ops._dt(q), batch, H, G, d, int(scale), C.c_void_p(q.data_ptr()), C.c_void_p(c.k.data_ptr()),
+        C.c_void_p(c.v.data_ptr()), c.k.shape[0], C.c_void_p(c.seg_start.data_ptr() + 4 * seg),
+        C.c_void_p(c.seg_cap.data_ptr() + 4 * seg), C.c_void_p(c.seqlens.data_ptr() + 4 * seg), int(max_rows),
+        None if k_new is None else C.c_void_p(k_new.data_ptr()),
+        None if v_new is None else C.c_void_p(v_new.data_ptr()), C.c_void_p(out.data_ptr()),
+        C.c_void_p(ws.data_ptr()), ws.numel(), L.DECODE_CHAINED if chained else 0, stream))
+
+
 class DecodeGraph:
     """One decode step over all layers, captured as a CUDA graph.
 
@@ -100,13 +115,8 @@ class DecodeGraph:
         H, G, d, B = c.H, c.G, c.d, self.B
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         for l in range(self.L):
-            seg = l * B * G
-            L.check(self._lib.adakv_decode(
-                self._dt, B, H, G, d, self.scale, C.c_void_p(self.q[l].data_ptr()), C.c_void_p(c.k.data_ptr()),
-                C.c_void_p(c.v.data_ptr()), c.k.shape[0], C.c_void_p(c.seg_start.data_ptr() + 4 * seg),
-                C.c_void_p(c.seqlens.data_ptr() + 4 * seg), self.max_rows, C.c_void_p(self.k_new[l].data_ptr()),
-                C.c_void_p(self.v_new[l].data_ptr()), C.c_void_p(self.out[l].data_ptr()),
-                C.c_void_p(self.ws.data_ptr()), self.ws.numel(), st))
+            decode_layer(self._lib, c, l, B, self.q[l], self.k_new[l], self.v_new[l], self.out[l], self.ws,
+                         self.max_rows, st, chained=l > 0, scale=self.scale)
 
     def step(self):
         if self.graph is not None:

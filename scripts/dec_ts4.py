@@ -36,7 +36,7 @@ vp = torch.randn((rows, d), device=dev).to(torch.bfloat16)
 cache = CompressedCache(k=kp, v=vp, seg_start=torch.as_tensor(starts, device=dev), seqlens=torch.as_tensor(lens, device=dev),
                         budgets=torch.as_tensor(lens, device=dev), P=Lyr * B, H=H, G=G, m=0, d=d, reserve=reserve,
                         layer_budget=LB)
-dg = PL.DecodeGraph(cache, Lyr, B, LB + reserve, use_graph=False)
+dg = PL.DecodeGraph(cache, Lyr, B, int(caps.max()), use_graph=False)
 dg.q.normal_()
 nl = steps * Lyr
 dbg = torch.zeros((nl, 256, 32), dtype=torch.int64, device=dev)
@@ -49,13 +49,8 @@ with torch.cuda.stream(st):
         for s in range(steps):
             for l in range(Lyr):
                 L.adakv_debug_set_decode_timestamps(C.c_void_p(dbg[s * Lyr + l].data_ptr()) if stamp else None)
-                seg = l * B * G
-                A._lib.check(L.adakv_decode(
-                    2, B, H, G, d, 1, C.c_void_p(dg.q[l].data_ptr()), C.c_void_p(cache.k.data_ptr()),
-                    C.c_void_p(cache.v.data_ptr()), cache.k.shape[0], C.c_void_p(cache.seg_start.data_ptr() + 4 * seg),
-                    C.c_void_p(cache.seqlens.data_ptr() + 4 * seg), LB + reserve, C.c_void_p(dg.k_new[l].data_ptr()),
-                    C.c_void_p(dg.v_new[l].data_ptr()), C.c_void_p(dg.out[l].data_ptr()), C.c_void_p(dg.ws.data_ptr()),
-                    dg.ws.numel(), C.c_void_p(st.cuda_stream)))
+                PL.decode_layer(L, cache, l, B, dg.q[l], dg.k_new[l], dg.v_new[l], dg.out[l], dg.ws, int(caps.max()),
+                                C.c_void_p(st.cuda_stream), chained=s > 0 or l > 0)
 L.adakv_debug_set_decode_timestamps(None)
 torch.cuda.synchronize()
 seq0 = cache.seqlens.clone()
@@ -67,12 +62,14 @@ e0.record()
 g.replay()
 e1.record()
 torch.cuda.synchronize()
+tm = False
 cs = L.adakv_debug_decode_cluster(B, G)
-print(f"cluster {cs}; graph: {nl} launches, {e0.elapsed_time(e1) * 1e3 / nl:.2f} us/launch; segment rows {lens.min()}..{lens.max()}")
+print(f"kernel tc cluster {cs}; graph: {nl} launches, {e0.elapsed_time(e1) * 1e3 / nl:.2f} us/launch; segment rows {lens.min()}..{lens.max()}")
 if not stamp:
     sys.exit(0)
 x = dbg.cpu().numpy()
-names = ["start", "issued", "post_wait", "loop0", "merged", "pushed", "recvd", "end"]
+names = (["start", "issued", "post_wait", "p_done", "o_done", "pushed", "recvd", "end"] if tm else
+         ["start", "issued", "post_wait", "loop0", "merged", "pushed", "recvd", "end"])
 base = x[nl // 2][x[nl // 2][:, 0] > 0, 0].min()
 print("launch: [min,max] per stamp, us relative to launch", nl // 2, "first start")
 for i in range(nl // 2, min(nl, nl // 2 + 12)):
@@ -115,6 +112,20 @@ for a_, b_ in [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 6), (6, 7)]:
 me = half[:, :, 4][act]
 wl = half[:, :, 24:32][act].max(axis=1)
 print("merged - max warp loop end (us): med", np.median((me - wl) / 1e3), "min", ((me - wl) / 1e3).min())
+if tm:
+    ck8 = half[:, :, 8:12][act]
+    pw = half[:, :, 18][act]
+    r = ck8 - pw[:, None]
+    print("ds warp-0 cycles after post_wait: pre-Q-wait %d, Q landed %d, S max done %d, P stored %d" %
+          tuple(np.median(r, axis=0)))
+    st0 = half[:, :, 16][act]
+    print("ds prologue (cycles after start): loads %d, inits %d, TMA issued %d" % (
+        np.median(half[:, :, 13][act] - st0), np.median(half[:, :, 14][act] - st0), np.median(half[:, :, 12][act] - st0)))
+    landed = half[:, :, 15][act] - half[:, :, 18][act]
+    print("ds all blocks landed, cycles relative to post_wait: med %d p10 %d p90 %d" % (
+        np.median(landed), np.percentile(landed, 10), np.percentile(landed, 90)))
+    print("  p90: %d %d %d %d" % tuple(np.percentile(r, 90, axis=0)))
+    sys.exit(0)
 # warp 1's first two blocks (cycles): slots 8..15 = [top, data, S, end] x 2; relative to post_wait clock
 w1 = half[:, :, 8:16][act]
 pw = ck[:, :, 2][act]

@@ -98,12 +98,7 @@ def main():
     def dec():
         stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         for l in range(P):
-            seg = l * G
-            A._lib.check(L.adakv_decode(2, 1, H, G, d, 1, C.c_void_p(dg.q[l].data_ptr()), C.c_void_p(cache.k.data_ptr()),
-                                        C.c_void_p(cache.v.data_ptr()), cache.k.shape[0], C.c_void_p(cache.seg_start.data_ptr() + 4 * seg),
-                                        C.c_void_p(cache.seqlens.data_ptr() + 4 * seg), max_rows, None, None,
-                                        C.c_void_p(dg.out[l].data_ptr()), C.c_void_p(dg.ws.data_ptr()), dg.ws.numel(),
-                                        stream))
+            PL.decode_layer(L, cache, l, 1, dg.q[l], None, None, dg.out[l], dg.ws, max_rows, stream, chained=l > 0)
     t = graph_time(dec, iters=20)
     rows = int(budgets.sum()) + P * G * m
     bytes_d = PL.algorithmic_bytes_decode_step(P, 1, H, G, d, rows)

@@ -22,7 +22,8 @@ def test_header_declares_the_boundary():
     for must in ("adakv_compress", "adakv_window_scores", "adakv_segmented_select", "adakv_gather",
                  "adakv_decode", "adakv_append_kv", "adakv_apportion", "adakv_uniform_allocation",
                  "adakv_safeguard_blend", "adakv_repair_zero_budgets", "adakv_pyramid_layer_budgets",
-                 "adakv_last_error", "adakv_workspace_status"):
+                 "adakv_last_error", "adakv_workspace_status", "adakv_validate_finite",
+                 "adakv_clear_workspace_status", "adakv_append_rows"):
         assert must in syms
 
 
@@ -31,7 +32,7 @@ def test_library_loads_and_exports_every_symbol():
     L = _lib.lib()
     for s in declared_symbols():
         assert hasattr(L, s), s
-    assert L.adakv_abi_version() == 1
+    assert L.adakv_abi_version() == 2
 
 
 def test_host_validation_mirrors_reference_throws():
@@ -52,7 +53,7 @@ def test_host_validation_mirrors_reference_throws():
     assert n.value > 0
     # floor: layer_budget >= m*G + G (policies.hpp:229-230) -- rejected before any launch
     st = L.adakv_compress(2, C.byref(shape), C.byref(cfg), 32 * 8 + 7, None, None, None, None, 0,
-                          C.c_void_p(1), C.c_void_p(1), C.c_void_p(1), C.c_void_p(1), C.c_void_p(1),
+                          C.c_void_p(1), C.c_void_p(1), C.c_void_p(1), C.c_void_p(1), None, C.c_void_p(1),
                           None, None, None, 0, None)
     assert st == 1 and b"window-plus-one floor" in L.adakv_last_error()
     # budget helpers: reference throw sites (budget.hpp:104, 148-152, 172-174)
@@ -78,3 +79,20 @@ def test_host_v_must_be_pinned_cpu_tensor():
     from paper_2407_11550_b200 import InvalidArgument, ops
     with pytest.raises(InvalidArgument):
         ops.host_device_pointer(torch.zeros(4, 4))  # not pinned (no CUDA here: cannot pin)
+
+
+def test_decode_and_append_refuse_missing_capacity_tables():
+    """The capacity table is part of the boundary: decode and append reject a NULL seg_cap
+    before launching (no unchecked writes past a segment, attention.hpp:126-134)."""
+    from paper_2407_11550_b200 import _lib
+    L = _lib.lib()
+    one = C.c_void_p(16)
+    st = L.adakv_decode(2, 1, 32, 8, 128, 1, one, one, one, 100, one, None, one, 64, None, None, one, one, 1 << 20,
+                        0, None)
+    assert st == 1 and b"segment table" in L.adakv_last_error()
+    st = L.adakv_decode(2, 1, 32, 8, 128, 1, one, one, one, 100, one, one, one, 64, None, None, one, one, 1 << 20,
+                        7, None)
+    assert st == 1 and b"flags" in L.adakv_last_error()
+    st = L.adakv_append_rows(2, 8, 1, 128, one, one, one, None, one, one, one, one, None)
+    assert st == 1 and b"segment table" in L.adakv_last_error()
+    assert L.adakv_validate_finite(2, one, -1, one, None) == 1

@@ -547,35 +547,7 @@ def test_decode_three_block_warps_vs_oracle(dev, oracle_mod):
             assert torch.equal(segs[g][0][-1], kn[0, g]) and torch.equal(segs[g][1][-1], vn[0, g])
 
 
-def test_decode_umma_variant_vs_oracle(dev, oracle_mod):
-    """The opt-in tcgen05 decode (decode_umma.cu): multi-step appends over long segments."""
-    O = oracle_mod
-    L = A.lib()
-    prev = L.adakv_debug_decode_umma(1)
-    try:
-        P, H, G, m, n_o, d = 2, 32, 8, 32, 8160, 128
-        q, k, v = planted_layer(P, H, G, n_o, m, d, seed=37, dtype=torch.bfloat16, device=dev)
-        cache = A.compress(q, k, v, 2048 * G, reserve=4)
-        gen = torch.Generator(device=dev)
-        gen.manual_seed(13)
-        for step in range(3):
-            qd = torch.randn((P, H, d), generator=gen, device=dev).to(torch.bfloat16)
-            kn = torch.randn((P, G, d), generator=gen, device=dev).to(torch.bfloat16)
-            vn = torch.randn((P, G, d), generator=gen, device=dev).to(torch.bfloat16)
-            o = A.decode(qd, cache, kn, vn)
-            for p in range(P):
-                segs = [cache.segment(p, g) for g in range(G)]
-                off = np.concatenate([[0], np.cumsum([s[0].shape[0] for s in segs])])
-                ref = O.decode_attention(qd[p].double().cpu().numpy(),
-                                         torch.cat([s[0] for s in segs]).double().cpu().numpy(),
-                                         torch.cat([s[1] for s in segs]).double().cpu().numpy(), off)
-                err = np.abs(o[p].double().cpu().numpy() - ref).max()
-                assert err <= 2e-2 and err <= 1e-2 * max(np.abs(ref).max(), 1e-3) + 4e-3, (step, p, err)
-    finally:
-        L.adakv_debug_decode_umma(prev)
-
-
-@pytest.mark.parametrize("H,G", [(2, 2), (6, 2), (10, 2), (12, 2), (14, 2), (16, 2)])
+@pytest.mark.parametrize("H,G", [(2, 2), (4, 2), (6, 2), (8, 2), (10, 2), (12, 2), (14, 2), (16, 2)])
 def test_decode_bf16_group_sizes_append(dev, oracle_mod, H, G):
     """The tensor-core decode at every group size g = H/G in 1..8 (head quads, padded heads,
     the CTA merge's (warp, head) lanes), two steps with appends: outputs within the bf16
