@@ -89,8 +89,9 @@ def test_config4_llama70b_64k_group_sharded_merge(dev, oracle_mod):
     r = kv_group_sharded_allocation(cache.scores[0], 0, G, LB - m * G, 0.2, CudaSelector())
     assert r.budgets.tolist() == cache.budgets.cpu().tolist()
     keep = cache.keep[0].cpu().numpy()
+    kept = r.kept(0, G)
     for g in range(G):
-        assert r.kept[g].tolist() == np.nonzero(keep[g])[0].tolist()
+        assert kept[g].tolist() == np.nonzero(keep[g])[0].tolist()
 
 
 def test_config5_question_agnostic_batch4(dev, oracle_mod):

@@ -19,25 +19,29 @@ from paper_2407_11550_b200.sharding import batch_shard, kv_group_sharded_allocat
 
 
 class OracleSelector:
+    """The same three primitives as CudaSelector, computed by the C oracle on the host."""
+
     def __init__(self):
         from oracle import oracle as O
         self.O = O
 
-    def local_topk(self, scores, k):
+    def topk(self, scores, k):
         rows = [r.astype(np.float64) for r in scores.float().numpy()]
         raw = self.O.adaptive_allocation(rows, k)
-        return [np.nonzero(self.O.topk_decision(rows[g], int(raw[g])))[0] for g in range(len(rows))]
+        pos = [np.nonzero(self.O.topk_decision(rows[g], int(raw[g])))[0] for g in range(len(rows))]
+        return torch.as_tensor(raw, dtype=torch.int32), torch.as_tensor(np.concatenate(pos), dtype=torch.int32)
 
-    def union_counts(self, rows, total):
-        return self.O.adaptive_allocation(list(rows), total)
+    def allocate(self, union, total, alpha, blend):
+        rows = [r.astype(np.float64) for r in union.float().numpy()]
+        raw = self.O.adaptive_allocation(rows, total)
+        caps = np.full(len(rows), union.shape[1], np.int64)
+        b = self.O.repair_zero_budgets(self.O.safeguard_blend(raw, total, len(raw), alpha, caps), caps) if blend else raw
+        return torch.as_tensor(raw, dtype=torch.int32), torch.as_tensor(b, dtype=torch.int32)
 
-    def blend_repair(self, raw, total, alpha, caps):
-        b = self.O.safeguard_blend(raw, total, len(raw), alpha, caps)
-        return self.O.repair_zero_budgets(b, caps)
-
-    def given_topk(self, scores, budgets):
+    def given(self, scores, budgets):
         rows = [r.astype(np.float64) for r in scores.float().numpy()]
-        return [np.nonzero(self.O.topk_decision(rows[g], int(budgets[g])))[0] for g in range(len(rows))]
+        pos = [np.nonzero(self.O.topk_decision(rows[g], int(budgets[g])))[0] for g in range(len(rows))]
+        return torch.as_tensor(np.concatenate(pos), dtype=torch.int32)
 
 
 def _free_port():
@@ -70,7 +74,8 @@ def _worker(rank, world, port, cases, out_q):
         gl = G // world
         local = torch.as_tensor(s[rank * gl:(rank + 1) * gl])
         r = kv_group_sharded_allocation(local, rank * gl, G, total, alpha, sel)
-        res.append((r.raw.tolist(), r.budgets.tolist(), [k.tolist() for k in r.kept]))
+        res.append((r.raw.tolist(), r.budgets.tolist(), [k.tolist() for k in r.kept(rank * gl, gl)],
+                    r.payload_bytes))
     out_q.put((rank, res))
     dist.barrier()
     dist.destroy_process_group()
@@ -100,7 +105,8 @@ def test_kv_group_sharded_matches_single_process(oracle_mod):
         keep = [np.nonzero(O.topk_decision(s[g], int(b[g])))[0].tolist() for g in range(G)]
         gl = G // world
         for rank in range(world):
-            r_raw, r_b, r_kept = results[rank][ci]
+            r_raw, r_b, r_kept, nbytes = results[rank][ci]
+            assert nbytes == 4 * (gl + 2 * min(total, gl * n))  # one fixed-size payload per rank
             assert r_raw == raw.tolist(), (ci, rank)
             assert r_b == b.tolist(), (ci, rank)
             assert r_kept == keep[rank * gl:(rank + 1) * gl], (ci, rank)
@@ -126,5 +132,40 @@ def test_kv_group_sharded_cuda_selector_single_rank(dev, oracle_mod):
     raw = O.adaptive_allocation(list(s64), total)
     b = O.repair_zero_budgets(O.safeguard_blend(raw, total, G, 0.2, np.full(G, n)), np.full(G, n))
     assert r.raw.tolist() == raw.tolist() and r.budgets.tolist() == b.tolist()
+    kept = r.kept(0, G)
     for g in range(G):
-        assert r.kept[g].tolist() == np.nonzero(O.topk_decision(s64[g], int(b[g])))[0].tolist()
+        assert kept[g].tolist() == np.nonzero(O.topk_decision(s64[g], int(b[g])))[0].tolist()
+
+
+@pytest.mark.gpu
+def test_kv_group_sharded_compress_nccl_world1(dev, oracle_mod, capfd):
+    """The KV-group-sharded compress through a real NCCL communicator (world size 1 on this
+    one-GPU box: the all-gather runs through NCCL) equals the single-GPU compress: budgets,
+    segment layout and every retained row bit for bit (Llama-3.1-70B shapes, g = 8, 8K prompt)."""
+    import paper_2407_11550_b200 as A
+    from paper_2407_11550_b200.sharding import compress_kv_group_sharded
+    from paper_2407_11550_b200.synthetic import planted_layer
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(_free_port()))
+    os.environ["NCCL_DEBUG"] = "INFO"
+    created = not dist.is_initialized()
+    if created:
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        H, G, m, n_o, d = 64, 8, 32, 8160, 128
+        q, k, v = planted_layer(1, H, G, n_o, m, d, seed=44, dtype=torch.bfloat16, device=dev)
+        LB = 512 * G
+        ref = A.compress(q, k, v, LB, reserve=3)
+        sh, alloc = compress_kv_group_sharded(q[0], k[0], v[0], LB, G, g0=0, reserve=3)
+        torch.cuda.synchronize()
+        assert alloc.budgets.cpu().tolist() == ref.budgets.cpu().tolist()
+        assert alloc.payload_bytes == 4 * (G + 2 * (LB - m * G))
+        for g in range(G):
+            a, b = sh.segment(0, g), ref.segment(0, g)
+            assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]), g
+        assert sh.seg_cap.cpu().tolist() == ref.seg_cap.cpu().tolist()
+    finally:
+        if created:
+            dist.destroy_process_group()
+    err = capfd.readouterr()
+    print("\n".join(l for l in (err.out + err.err).splitlines() if "NCCL INFO" in l and ("comm" in l or "Init" in l))[:2000])
