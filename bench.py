@@ -21,8 +21,12 @@ the current compress + decode).  decode_batch_scaling (supplementary): the decod
 batch 1 and 8 on synthetic caches of this shape.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-Multi-GPU (torchrun): independent requests shard by batch, one per rank (weak scaling,
-no data-path collective).
+Multi-GPU: `--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU, NCCL).  The headline workload shards by
+batch, one config-2 request per rank (weak scaling, no data-path collective); the config3
+field splits config 3's 8 requests over the ranks (strong scaling, no collective) and the
+config4 field splits config 4's 8 KV groups over the ranks with one NCCL all-gather per
+layer (scripts/bench_configs.py).
 """
 from __future__ import annotations
 
@@ -275,6 +279,18 @@ def decode_batch_scaling(dev, H, G, d, L, budget_rows, batches=(1, 8), steps=4, 
         del g, dg, cache, kp, vp, dq, dk
         torch.cuda.empty_cache()
     return res
+
+
+def relaunch(args) -> int:
+    """`--gpus N` outside torchrun: re-exec this script under torch.distributed.run, N ranks."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def run_ours(args, cfg):
@@ -557,6 +573,11 @@ def run_ours(args, cfg):
             "batch": sorted(scal), "us_per_launch": [round(scal[b][0], 3) for b in sorted(scal)],
             "gbs": [round(scal[b][1], 1) for b in sorted(scal)],
             "frac": [round(scal[b][1] / pk, 4) for b in sorted(scal)]}
+    if not args.no_configs:
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        import bench_configs as BC
+        line["config3"] = BC.config3(dev, peak, rank, ws)
+        line["config4"] = BC.config4(dev, peak, rank, ws)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         try:
@@ -589,7 +610,10 @@ def main():
     ap.add_argument("--prompt", type=int)
     ap.add_argument("--decode-steps", type=int)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the config3 / config4 fields")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return relaunch(args)
     cfg = dict(CONFIGS[args.config])
     if args.layers:
         cfg["layers"] = args.layers

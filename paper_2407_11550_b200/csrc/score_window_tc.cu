@@ -76,7 +76,10 @@ struct __align__(1024) Smem {
 
 struct TcParams {
     int pass;
-    int G, H, gs, m, n_o, step, pad;
+    // a group of g*m > 128 window rows (Llama-70B: 8 x 32) is scored as vsplit UMMA tiles of
+    // gs = g / vsplit heads each over the same K ("virtual groups": pg counts them); their
+    // group-score halves are added into the zeroed output (two addends: order-independent)
+    int G, H, gs, vsplit, m, n_o, step, pad;
     int tiles_per_pg, tiles_per_item, chunks_per_pg, n_items;
     int pg_base;
     int debug;  // (experiments) 1: pass 1 only; 4/8/16: skip ticket / fences / fold; 64: MUFU-only exp2 in pass 1
@@ -273,8 +276,8 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                     prod_wait += clock64() - w0;
                     mbar_arrive_expect_tx(&S.full[stage], kTileBytes);
                     const int row = t * prm.step - prm.pad;
-                    tma_load_3d(S.k[stage][0], &tm_k, 0, row, pg, &S.full[stage], pol);
-                    tma_load_3d(S.k[stage][1], &tm_k, 64, row, pg, &S.full[stage], pol);
+                    tma_load_3d(S.k[stage][0], &tm_k, 0, row, pg / prm.vsplit, &S.full[stage], pol);
+                    tma_load_3d(S.k[stage][1], &tm_k, 64, row, pg / prm.vsplit, &S.full[stage], pol);
                     if (++stage == kStages) {
                         stage = 0;
                         sphase ^= 1;
@@ -389,8 +392,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             const int o = q * 32 + lane;
             const int key = rt * prm.step + o;
             if (o < prm.step && key < prm.n_o) {
-                const int gpg = prm.pg_base + rpg;
-                const int p = gpg / prm.G, g = gpg % prm.G;
+                const int gpg = prm.pg_base + rpg;           // virtual group
+                const int gvirt = prm.G * prm.vsplit;
+                const int p = gpg / gvirt, gv = gpg % gvirt;
+                const int g = gv / prm.vsplit, h0 = (gv % prm.vsplit) * prm.gs;  // first head of the tile
                 constexpr float inv_scale = 1.f / 65536.f;
                 float gsum = 0.f;
 #pragma unroll
@@ -399,9 +404,11 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                     const float sh = hv[h] * inv_scale;
                     gsum += sh;
                     if (prm.head_scores)
-                        prm.head_scores[(size_t(p) * prm.H + g * prm.gs + h) * prm.n_o + key] = sh;
+                        prm.head_scores[(size_t(p) * prm.H + g * prm.gs * prm.vsplit + h0 + h) * prm.n_o + key] = sh;
                 }
-                prm.group_scores[size_t(gpg) * prm.n_o + key] = gsum * prm.inv_g;
+                float* gdst = prm.group_scores + (size_t(p) * prm.G + g) * prm.n_o + key;
+                if (prm.vsplit == 1) *gdst = gsum * prm.inv_g;
+                else atomicAdd(gdst, gsum * prm.inv_g);
             }
         };
         for (int item = blockIdx.x; item < prm.n_items; item += gridDim.x) {
@@ -601,12 +608,16 @@ struct Plan {
     int tpi1, chunks1, tpi2, chunks2;
 };
 
+}  // namespace
+int vsplit_of(const adakv_layer_shape& s);
+namespace {
+
 Plan make_plan(const adakv_layer_shape& s, int pad) {
     Plan pl{};
     const int64_t k_bytes = s.kv_groups * (s.outside + s.window) * s.head_dim * 2;
     pl.slice = std::max<int64_t>(1, std::min<int64_t>(s.problems, (48ll << 20) / std::max<int64_t>(k_bytes, 1)));
     const int sms = device_sm_count();
-    const int64_t pgs = pl.slice * s.kv_groups;
+    const int64_t pgs = pl.slice * s.kv_groups * std::max(1, vsplit_of(s));
     balance(pgs, ceil_div(s.outside, kTile), sms, &pl.tpi1, &pl.chunks1);
     balance(pgs, ceil_div(s.outside, kTile - 2 * pad), sms, &pl.tpi2, &pl.chunks2);
     return pl;
@@ -614,18 +625,28 @@ Plan make_plan(const adakv_layer_shape& s, int pad) {
 
 }  // namespace
 
+// window-row tiles per KV group: 1 while g*m <= 128; else the smallest split into <= 128-row
+// tiles of whole heads (g = 8, m = 32 -> 2)
+int vsplit_of(const adakv_layer_shape& s) {
+    const int64_t gs = s.kv_groups > 0 ? s.q_heads / s.kv_groups : 0;
+    for (int v = 1; v <= 4; v *= 2)
+        if (gs % v == 0 && (gs / v) * s.window <= 128) return v;
+    return 0;
+}
+
 bool score_window_tc_supported(adakv_dtype dt, const adakv_layer_shape& s, int64_t pool_kernel) {
     const int64_t gs = s.kv_groups > 0 ? s.q_heads / s.kv_groups : 0;
-    return dt == ADAKV_BF16 && s.head_dim == 128 && s.window == 32 && gs >= 1 && gs * s.window <= 128 &&
+    return dt == ADAKV_BF16 && s.head_dim == 128 && s.window == 32 && gs >= 1 && vsplit_of(s) > 0 &&
            (pool_kernel == 1 || pool_kernel == 3 || pool_kernel == 5 || pool_kernel == 7) && s.outside >= 1 &&
            s.outside + s.window < (int64_t(1) << 31) && ptx::get_encode() != nullptr;
 }
 
 size_t score_window_tc_workspace(const adakv_layer_shape& s) {
     const Plan pl = make_plan(s, 0);
-    const int64_t pgs_slice = pl.slice * s.kv_groups;
+    const int64_t vs = std::max(1, vsplit_of(s));
+    const int64_t pgs_slice = pl.slice * s.kv_groups * vs;
     return 3 * 256 + size_t(pgs_slice) * pl.chunks1 * 4 * 128 * 2 * 4 +
-           size_t(s.problems * s.kv_groups) * 128 * 2 * 4 + size_t(pgs_slice) * 4;
+           size_t(s.problems * s.kv_groups * vs) * 128 * 2 * 4 + size_t(pgs_slice) * 4;
 }
 
 adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, int32_t scale, const void* q,
@@ -635,11 +656,14 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
     const Plan pl = make_plan(s, pad);
     const int64_t G = s.kv_groups, H = s.q_heads, gs = H / G, m = s.window, n = s.outside + s.window;
     const int64_t d = s.head_dim;
+    const int64_t vs = vsplit_of(s), Gv = G * vs, gst = gs / vs;  // virtual groups of gst heads
     Arena ar(ws);
-    float* partial = ar.take<float>(size_t(pl.slice * G * pl.chunks1 * 4 * 256));
-    float* fstats = ar.take<float>(size_t(s.problems * G * 256));
-    unsigned* tickets = ar.take<unsigned>(size_t(pl.slice * G));
-    ADAKV_CUDA_TRY(cudaMemsetAsync(tickets, 0, size_t(pl.slice * G) * 4, stream));
+    float* partial = ar.take<float>(size_t(pl.slice * Gv * pl.chunks1 * 4 * 256));
+    float* fstats = ar.take<float>(size_t(s.problems * Gv * 256));
+    unsigned* tickets = ar.take<unsigned>(size_t(pl.slice * Gv));
+    ADAKV_CUDA_TRY(cudaMemsetAsync(tickets, 0, size_t(pl.slice * Gv) * 4, stream));
+    if (vs > 1)  // the virtual groups' halves are added into the group scores
+        ADAKV_CUDA_TRY(cudaMemsetAsync(group_scores, 0, size_t(s.problems * G * s.outside) * 4, stream));
     const size_t smem = smem_bytes();
     const int sms = device_sm_count();
     auto k2 = pad == 0 ? score_tc_kernel<0> : pad == 1 ? score_tc_kernel<1> : pad == 2 ? score_tc_kernel<2>
@@ -652,15 +676,16 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
         CUtensorMap tq, tk;
         const auto* qb = static_cast<const __nv_bfloat16*>(q) + p0 * H * m * d;
         const auto* kb = static_cast<const __nv_bfloat16*>(k) + p0 * G * n * d;
-        ADAKV_TRY(make_map(&tq, qb, uint64_t(gs * m), uint64_t(np * G)));
+        ADAKV_TRY(make_map(&tq, qb, uint64_t(gst * m), uint64_t(np * Gv)));
         ADAKV_TRY(make_map(&tk, kb, uint64_t(n), uint64_t(np * G)));
         TcParams prm{};
         prm.G = int(G);
         prm.H = int(H);
-        prm.gs = int(gs);
+        prm.gs = int(gst);
+        prm.vsplit = int(vs);
         prm.m = int(m);
         prm.n_o = int(s.outside);
-        prm.pg_base = int(p0 * G);
+        prm.pg_base = int(p0 * Gv);
         prm.scale_log2 = sc * 1.4426950408889634f;
         prm.log2_m = log2f(float(m));
         prm.inv_g = 1.0f / float(gs);
@@ -683,7 +708,7 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
         prm.tiles_per_pg = int(ceil_div(s.outside, kTile));
         prm.tiles_per_item = pl.tpi1;
         prm.chunks_per_pg = pl.chunks1;
-        prm.n_items = int(np * G * prm.chunks_per_pg);
+        prm.n_items = int(np * Gv * prm.chunks_per_pg);
         int grid = std::min(prm.n_items, sms);
         cudaLaunchAttribute pdl[1];
         pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -703,7 +728,7 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
         prm.tiles_per_pg = int(ceil_div(s.outside, prm.step));
         prm.tiles_per_item = pl.tpi2;
         prm.chunks_per_pg = pl.chunks2;
-        prm.n_items = int(np * G * prm.chunks_per_pg);
+        prm.n_items = int(np * Gv * prm.chunks_per_pg);
         grid = std::min(prm.n_items, sms);
         if (dbg & 1) continue;  // debug: pass 1 only
         lc.gridDim = dim3(unsigned(grid));

@@ -82,10 +82,11 @@ def test_config3_every_request_scores(dev):
         assert e <= 1e-4, (p, e)
 
 
-@pytest.mark.parametrize("H,G", [(8, 8), (16, 8), (24, 8), (32, 8)])
+@pytest.mark.parametrize("H,G", [(8, 8), (16, 8), (24, 8), (32, 8), (64, 8)])
 def test_tc_scoring_group_sizes(dev, H, G):
     """The tcgen05 scoring kernel at g = H/G = 1, 2, 3, 4 (g*m = 32..128 window rows per
-    UMMA tile; rows past g*m are idle lanes), 4K prompt, every group."""
+    UMMA tile; rows past g*m are idle lanes) and g = 8 (Llama-70B: 256 window rows, scored as
+    two 128-row tiles over the same keys whose halves are added), 4K prompt, every group."""
     m, n_o, d = 32, 4064, 128
     q, k, v = planted_layer(2, H, G, n_o, m, d, seed=H, dtype=torch.bfloat16, device=dev)
     gs, hs = A.window_scores(q, k, 7, head_scores=True)
@@ -95,6 +96,18 @@ def test_tc_scoring_group_sizes(dev, H, G):
         # staging bound of the module docstring is what holds there
         assert _max_rel_err(gs[p], ref_g) <= (1e-4 if H // G > 1 else 5e-4), p
         assert _max_rel_err(hs[p], ref_h) <= 5e-4, p
+
+
+def test_config4_llama70b_scores_on_tensor_cores(dev):
+    """Config 4 (Llama-3.1-70B shapes: 64 Q / 8 KV heads, 64K prompt): every group's scores from
+    the tcgen05 path (g*m = 256 rows as two UMMA tiles) against the fp64 restatement."""
+    H, G, m, n_o, d = 64, 8, 32, 65504, 128
+    q, k, v = planted_layer(1, H, G, n_o, m, d, seed=41, dtype=torch.bfloat16, device=dev)
+    gs = A.window_scores(q, k, 7)
+    ref, _ = window_scores_f64(q[0], k[0], 7)
+    e = _max_rel_err(gs[0], ref)
+    print(f"config 4: max error / max score = {e:.2e}")
+    assert e <= 1e-4, e
 
 
 def test_coinciding_window_rows_fp16_staging_bound(dev):
