@@ -262,7 +262,11 @@ adakv_status adakv_decode(adakv_dtype dtype, int64_t problems, int64_t q_heads,
                           const void* v_new, void* out, void* workspace, size_t workspace_bytes,
                           uint32_t flags, adakv_stream_t stream);
 /* max_rows: upper bound of any segment length during this call (grid sizing; the
- * launch covers ceil(max_rows / chunk) splits so the call can live in a CUDA graph). */
+ * launch covers ceil(max_rows / chunk) splits so the call can live in a CUDA graph).
+ * The workspace must be zero-initialised before its first decode; the split-K kernels re-arm
+ * the per-segment tickets they keep in it, so it stays valid for further calls of the SAME
+ * (problems, q_heads, kv_groups, head_dim, max_rows) -- a call of another layout needs its own
+ * (or a re-zeroed) workspace. */
 adakv_status adakv_decode_workspace(int64_t problems, int64_t q_heads, int64_t kv_groups,
                                     int64_t head_dim, int64_t max_rows, size_t* bytes);
 

@@ -333,3 +333,51 @@ def bench_decode(q, k, v, off, threads, units):
     _call("ref", "bench_decode", P(q), P(k), P(v), P(off, I64), I64(H), I64(G), I64(d),
           C.c_int(threads), C.c_int(units), C.byref(secs))
     return secs.value
+
+
+# ---------------------------------------------------------------- run_comparison restated
+def _softmax_row(logits):
+    """masked_softmax_inplace over every entry (attention.hpp:141-157): max-subtracted, summed
+    in index order, then divided."""
+    mx = np.max(logits)
+    e = np.exp(logits - mx)
+    return e / np.sum(e)
+
+
+def comparison_row(q_win, k_out, v_out, k_win, v_win, q_dec, wo, layer_budget, kind="ada_snapkv", alpha=0.2,
+                   pool_kernel=7, impl="oracle"):
+    """One (sample, fraction, policy) row of run_comparison for a full trace with one layer and
+    no GQA (report.hpp:216-249): evict_layer's decision through the C restatement, then the
+    eviction-loss ladder of eviction_loss.hpp against the decode query's true weights (the
+    last window token's query over the full cache, make_sample_context report.hpp:104-127).
+    Shapes: q_win [h,m,d], k_out/v_out [h,n,d], k_win/v_win [h,m,d], q_dec [h,d], wo [h,d,D].
+    Returns dict(loss, epsilon, epsilon_star, epsilon_double_star, mass, alloc)."""
+    h, n, d = np.asarray(k_out).shape
+    m = np.asarray(k_win).shape[1]
+    res = evict_layer(q_win, k_out, v_out, k_win, v_win, layer_budget, kind=kind, pool_kernel=pool_kernel,
+                      alpha=alpha, impl=impl)
+    inv = 1.0 / np.sqrt(d)
+    keys = [np.concatenate([k_out[i], k_win[i]]) for i in range(h)]
+    vals = [np.concatenate([v_out[i], v_win[i]]) for i in range(h)]
+    true_w = [_softmax_row(keys[i] @ q_dec[i] * inv) for i in range(h)]
+    # attention_output (attention.hpp:182-196): y = sum_i (w_i V_i) W_i^O
+    y = sum((true_w[i] @ vals[i]) @ wo[i] for i in range(h))
+    # row_norm_constant (eviction_loss.hpp:26-41) over the full cache
+    c = max(np.abs(vals[i] @ wo[i]).sum(axis=1).max() for i in range(h))
+    keep = res.keep.reshape(h, n)
+    full_keep = [np.concatenate([keep[i], np.ones(m, np.uint8)]) for i in range(h)]
+    # y_hat: a fresh softmax over each head's retained rows (output_from_retained, report.hpp:130-141)
+    off = np.concatenate([[0], np.cumsum(res.ret_len)])
+    y_hat = 0.0
+    for i in range(h):
+        kr, vr = res.k_ret[off[i]:off[i + 1]], res.v_ret[off[i]:off[i + 1]]
+        y_hat = y_hat + (_softmax_row(kr @ q_dec[i] * inv) @ vr) @ wo[i]
+    evicted = sum(true_w[i][full_keep[i] == 0].sum() for i in range(h))
+    mass = sum(true_w[i][full_keep[i] != 0].sum() for i in range(h))
+    scores = res.group_scores.reshape(h, n)
+    alloc = np.asarray(res.alloc)
+    topk = lambda row, k: np.sort(row)[::-1][:k].sum() if k else 0.0  # noqa: E731
+    eps_s = 2.0 * (h - sum(topk(scores[i], int(alloc[i])) for i in range(h)))
+    eps_ss = 2.0 * (h - topk(scores.reshape(-1), int(alloc.sum())))
+    return {"loss": float(np.abs(y - y_hat).sum()), "epsilon": float(2.0 * c * evicted), "epsilon_star": float(eps_s),
+            "epsilon_double_star": float(eps_ss), "mass": float(mass), "alloc": alloc.copy()}

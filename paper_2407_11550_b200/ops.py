@@ -323,7 +323,10 @@ def decode(q: torch.Tensor, cache: CompressedCache, k_new: torch.Tensor | None =
         out = torch.empty_like(q)
     lib = L.lib()
     if ws is None:
-        ws = workspace(decode_workspace_bytes(P, H, cache.G, d, mr), q.device, "decode")
+        # the split-K kernels keep per-segment tickets in the workspace and re-arm them, so a
+        # workspace is reusable only by calls of the same layout: one cached workspace per
+        # (problems, heads, groups, d, max_rows), zeroed when first created
+        ws = workspace(decode_workspace_bytes(P, H, cache.G, d, mr), q.device, ("decode", P, H, cache.G, d, mr))
     L.check(lib.adakv_decode(_dt(q), P, H, cache.G, d, int(bool(scale)), _p(q), _p(cache.k), _p(cache.v),
                              cache.k.shape[0], _p(cache.seg_start), _p(cache.seg_cap), _p(cache.seqlens), mr,
                              _p(k_new), _p(v_new), _p(out), _p(ws), ws.numel(), 0, _stream()))

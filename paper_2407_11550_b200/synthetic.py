@@ -49,8 +49,14 @@ def planted_rows(G: int, n: int, gen: torch.Generator, frac_sparse=0.75, top_mas
 
 
 def planted_layer(P: int, H: int, G: int, n_o: int, m: int, d: int, seed: int = 7, dtype=torch.bfloat16,
-                  device="cpu"):
-    """Returns q [P,H,m,d], k [P,G,n_o+m,d], v [P,G,n_o+m,d] in `dtype` on `device`."""
+                  device="cpu", values="gaussian"):
+    """Returns q [P,H,m,d], k [P,G,n_o+m,d], v [P,G,n_o+m,d] in `dtype` on `device`.
+
+    values="gaussian": V ~ N(0, 1).  values="embedding": V = X W_v as the reference generator
+    forms it (trace.hpp:203-261): X's rows carry every group's key block (the planted log-weight
+    direction c_g,j u_g + 0.05 eps; window rows 0.1 eps) and every head's query block (window
+    rows only), W_v,g ~ N(0, 1/D), D = (G + H) d -- so a position's value is correlated with the
+    planted weights, as in the reference's traces.  (Small shapes only: X is [n_o + m, D].)"""
     gen = torch.Generator(device="cpu")
     gen.manual_seed(seed)
     dgen = torch.Generator(device=device)
@@ -70,4 +76,11 @@ def planted_layer(P: int, H: int, G: int, n_o: int, m: int, d: int, seed: int = 
         uq = u.repeat_interleave(g, dim=0)                                     # [H, d]
         qq = math.sqrt(d) * uq[:, None, :] + 0.15 * torch.randn((H, m, d), generator=dgen, device=device)
         q[p] = qq.to(dtype)
+        if values == "embedding":
+            D = (G + H) * d
+            x = torch.zeros((n_o + m, G + H, d), device=device)
+            x[:, :G] = torch.cat([kk, kw], dim=1).transpose(0, 1)             # key blocks
+            x[n_o:, G:] = qq.transpose(0, 1)                                  # query blocks (window rows)
+            wv = torch.randn((G, D, d), generator=dgen, device=device) / math.sqrt(D)
+            v[p] = torch.einsum("nD,gDe->gne", x.reshape(n_o + m, D), wv).to(dtype)
     return q, k, v

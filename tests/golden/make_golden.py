@@ -21,6 +21,14 @@ Fixtures:
   select_ties.npz  adversarial selection inputs (all-equal, quantised k/64,
                    underflowed zeros) with the reference's adaptive_allocation,
                    safeguard_blend and topk_decision results.
+  fig3_dump.npz    the reference's run_comparison (report.hpp:161-345) on a small
+                   trace of its own generator (h=8, n=256, d_h=4, 6 samples, seed 5):
+                   every sample's inputs (K/V, window queries, decode query, W_o) and
+                   the reference's rows (loss, epsilon, epsilon*, epsilon**, retained
+                   mass, allocation) for ada_snapkv / snapkv at fractions 0.2 / 0.4.
+  fig3_accept.npz  acceptance check #7 (acceptance_test.cpp:134-163) as the reference
+                   runs it: 200 samples, fractions 0.2 / 0.4 -- per-sample losses of
+                   both policies and the win fractions.
 """
 from __future__ import annotations
 
@@ -110,8 +118,62 @@ def select_ties():
     print("select_ties", len(dists), "distributions")
 
 
+def _parse_rows(path):
+    rows, aggs = [], []
+    for line in open(path):
+        t = line.split()
+        if t[0] == "agg":
+            aggs.append([float(t[1]), int(t[2]), int(t[3]), float(t[4])])
+        else:
+            rows.append((int(t[0]), float(t[1]), t[2], int(t[3]), [float(x) for x in t[4:9]],
+                         [int(x) for x in t[9:]]))
+    return rows, np.array(aggs)
+
+
+def fig3():
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "fig3"], check=True)
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_fig3")
+    h, n, d, m, S, D = 8, 256, 4, 32, 6, (8 + 8) * 4
+    with tempfile.TemporaryDirectory() as td:
+        subprocess.run([exe, "dump", td], check=True)
+        wo = np.fromfile(os.path.join(td, "wo.f64"), np.float64).reshape(h, d, D)
+        arrs = {k: [] for k in ("k_out", "v_out", "k_win", "v_win", "q_win", "q_dec")}
+        for si in range(S):
+            x = np.fromfile(os.path.join(td, f"s{si}.f64"), np.float64)
+            o = 0
+            for key, shape in (("k_out", (h, n, d)), ("v_out", (h, n, d)), ("k_win", (h, m, d)),
+                               ("v_win", (h, m, d)), ("q_win", (h, m, d)), ("q_dec", (h, d))):
+                cnt = int(np.prod(shape))
+                arrs[key].append(x[o:o + cnt].reshape(shape))
+                o += cnt
+            assert o == x.size
+        rows, aggs = _parse_rows(os.path.join(td, "rows.txt"))
+    out = {k: np.stack(v) for k, v in arrs.items()}
+    out["wo"] = wo
+    out["row_sample"] = np.array([r[0] for r in rows], np.int64)
+    out["row_fraction"] = np.array([r[1] for r in rows])
+    out["row_policy"] = np.array([r[2] for r in rows])
+    out["row_budget"] = np.array([r[3] for r in rows], np.int64)
+    out["row_values"] = np.array([r[4] for r in rows])      # loss, epsilon, eps*, eps**, mass
+    out["row_alloc"] = np.array([r[5] for r in rows], np.int64)
+    out["aggregates"] = aggs
+    np.savez_compressed(os.path.join(OUT, "fig3_dump.npz"), **out)
+    with tempfile.TemporaryDirectory() as td:
+        subprocess.run([exe, "accept", os.path.join(td, "a.txt")], check=True)
+        rows, aggs = _parse_rows(os.path.join(td, "a.txt"))
+    np.savez_compressed(os.path.join(OUT, "fig3_accept.npz"),
+                        sample=np.array([r[0] for r in rows], np.int64),
+                        fraction=np.array([r[1] for r in rows]), policy=np.array([r[2] for r in rows]),
+                        loss=np.array([r[4][0] for r in rows]), aggregates=aggs)
+    print("fig3: dump rows", len(out["row_sample"]), "accept win fractions", aggs[:, 3].tolist())
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "fig3":
+        fig3()
+        sys.exit(0)
     run_generator("config1", 32, 4, 4064, 128, 32, 7, 8192, "ada_snapkv", 0.2, 7)
     run_generator("demo", 4, 1, 256, 8, 8, 7, (256 + 8) * 4 // 4, "ada_snapkv", 0.2, 7)
     evict_small()
     select_ties()
+    fig3()

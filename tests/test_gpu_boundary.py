@@ -151,3 +151,20 @@ def test_per_problem_budgets_outside_floor_or_capacity(dev):
         b = bud.view(P, G).cpu()
         assert (b[2] == 0).all()  # the rejected problem: zero budgets, window rows only
         assert (sl.view(P, G).cpu()[2] == m).all()
+
+
+def test_decode_workspace_reuse_across_layouts(dev, oracle_mod):
+    """ops.decode's cached workspace: a split-K decode of a small batch, then one of a larger
+    batch (whose ticket words would land on the first call's partials) -- both exact."""
+    O = oracle_mod
+    for P in (3, 40, 3):
+        q, k, v = planted_layer(P, 8, 8, 300, 8, 16, seed=P, dtype=torch.float64, device=dev)
+        cache = A.compress(q, k, v, 64 * 8)
+        qd = q[:, :, -1, :].contiguous()
+        o = A.decode(qd, cache)
+        for p in (0, P - 1):
+            segs = [cache.segment(p, g) for g in range(8)]
+            off = np.concatenate([[0], np.cumsum([s[0].shape[0] for s in segs])])
+            ref = O.decode_attention(qd[p].cpu().numpy(), torch.cat([s[0] for s in segs]).cpu().numpy(),
+                                     torch.cat([s[1] for s in segs]).cpu().numpy(), off)
+            assert np.allclose(o[p].cpu().numpy(), ref, rtol=1e-10, atol=1e-12), (P, p)

@@ -39,3 +39,92 @@ def test_adaptive_retains_more_mass_than_uniform(dev):
     assert np.all(ra >= ru * (1 - 1e-6)), (ra, ru)
     la, lu = r["l1_ada"].cpu().numpy(), r["l1_uniform"].cpu().numpy()
     assert (la <= lu).mean() >= 0.5, (la, lu)
+
+
+KEYS = ("loss", "epsilon", "epsilon_star", "epsilon_double_star", "mass")
+
+
+def test_oracle_comparison_rows_pinned_to_reference(oracle_mod):
+    """oracle.comparison_row (C evict_layer + the eviction_loss.hpp ladder restated in numpy)
+    reproduces the reference's own run_comparison rows (report.hpp:216-249) on a trace of the
+    reference's generator: allocations exact, every metric to 1e-12 relative."""
+    from conftest import load_golden
+    O = oracle_mod
+    z = load_golden("fig3_dump.npz")
+    for r in range(len(z["row_sample"])):
+        s = int(z["row_sample"][r])
+        row = O.comparison_row(z["q_win"][s], z["k_out"][s], z["v_out"][s], z["k_win"][s], z["v_win"][s],
+                               z["q_dec"][s], z["wo"], int(z["row_budget"][r]), str(z["row_policy"][r]))
+        assert row["alloc"].tolist() == z["row_alloc"][r].tolist(), r
+        got = np.array([row[k] for k in KEYS])
+        assert np.allclose(got, z["row_values"][r], rtol=1e-12, atol=0), (r, got, z["row_values"][r])
+
+
+def test_bound_ladder_definitions(oracle_mod):
+    """epsilon_star / epsilon_double_star (eviction_loss.hpp:97-127) and row_norm_constant
+    (26-41) on torch tensors equal the direct formulas."""
+    rng = np.random.default_rng(5)
+    w = rng.random((3, 4, 50))
+    b = rng.integers(0, 51, size=(3, 4))
+    es = quality.epsilon_star(torch.as_tensor(w), torch.as_tensor(b), 1.5).numpy()
+    ref = [2 * 1.5 * (4 - sum(np.sort(w[p, i])[::-1][:b[p, i]].sum() for i in range(4))) for p in range(3)]
+    assert np.allclose(es, ref, rtol=1e-13)
+    ess = quality.epsilon_double_star(torch.as_tensor(w), torch.as_tensor(b.sum(axis=1)), 2.0).numpy()
+    ref = [2 * 2.0 * (4 - np.sort(w[p].ravel())[::-1][:b[p].sum()].sum()) for p in range(3)]
+    assert np.allclose(ess, ref, rtol=1e-13)
+    v, wo = rng.normal(size=(4, 30, 8)), rng.normal(size=(4, 8, 16))
+    c = max(np.abs(v[i] @ wo[i]).sum(axis=1).max() for i in range(4))
+    assert np.isclose(quality.row_norm_constant(torch.as_tensor(v), torch.as_tensor(wo)), c, rtol=1e-13)
+
+
+@pytest.mark.gpu
+def test_device_comparison_rows_match_reference(dev):
+    """quality.comparison_rows on the reference generator's trace, through the device's fp64
+    path (compress -> decode over the compressed cache): the reference's rows."""
+    from conftest import load_golden
+    z = load_golden("fig3_dump.npz")
+    T = lambda x: torch.as_tensor(x, device=dev)  # noqa: E731
+    cells = sorted({(float(f), str(p), int(b)) for f, p, b in zip(z["row_fraction"], z["row_policy"], z["row_budget"])})
+    assert len(cells) == 4
+    for f, pol, LB in cells:  # every sample of one (fraction, policy) cell in one device call
+        sel = [i for i in range(len(z["row_sample"]))
+               if float(z["row_fraction"][i]) == f and str(z["row_policy"][i]) == pol]
+        ss = [int(z["row_sample"][i]) for i in sel]
+        out = quality.comparison_rows(T(z["q_win"][ss]), T(z["k_out"][ss]), T(z["v_out"][ss]), T(z["k_win"][ss]),
+                                      T(z["v_win"][ss]), T(z["q_dec"][ss]), T(z["wo"]), LB, kind=pol)
+        for j, i in enumerate(sel):
+            assert out["alloc"][j].cpu().tolist() == z["row_alloc"][i].tolist(), (f, pol, j)
+            got = np.array([float(out[k][j]) for k in KEYS])
+            assert np.allclose(got, z["row_values"][i], rtol=1e-9, atol=0), (f, pol, j, got, z["row_values"][i])
+
+
+@pytest.mark.gpu
+def test_fig3_adaptive_beats_uniform_on_device(dev, oracle_mod):
+    """The Fig.-3 / acceptance #7 analogue on the device: 200 planted samples (8 heads, 512
+    outside positions, window 32, d = 8, values formed from the planted embedding as the
+    reference generator forms them; fp64 device path), ada_snapkv vs snapkv at budget
+    fractions 0.2 / 0.4 -- the adaptive policy's loss is lower on >= 90% of samples at both
+    (the reference's own run on its generator: 100% / 99.5%, tests/golden/fig3_accept.npz), and
+    every device row equals the oracle's comparison_row on the same inputs."""
+    from conftest import load_golden
+    from paper_2407_11550_b200.synthetic import planted_layer
+    O = oracle_mod
+    ref = load_golden("fig3_accept.npz")["aggregates"]
+    assert ref[:, 3].min() >= 0.9
+    P, H, G, m, n, d, D = 200, 8, 8, 32, 512, 8, 128
+    q, k, v = planted_layer(P, H, G, n, m, d, seed=71, dtype=torch.float64, device=dev, values="embedding")
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(3)
+    wo = torch.randn((H, d, D), generator=gen, device=dev, dtype=torch.float64) / d ** 0.5
+    args = (q, k[:, :, :n], v[:, :, :n], k[:, :, n:], v[:, :, n:], q[:, :, m - 1, :], wo)
+    rows, agg = quality.run_comparison(*args, fractions=(0.2, 0.4))
+    print(f"device win fractions {agg}; reference {ref[:, 3].tolist()}")
+    h = [x.cpu().numpy() for x in args]
+    for (f, pol), row in rows.items():
+        LB = int(np.ceil(f * G * (n + m)))
+        for s in range(0, P, 7):
+            o = O.comparison_row(h[0][s], h[1][s], h[2][s], h[3][s], h[4][s], h[5][s], h[6], LB, pol)
+            assert row["alloc"][s].cpu().tolist() == o["alloc"].tolist(), (f, pol, s)
+            got = np.array([float(row[kk][s]) for kk in KEYS])
+            assert np.allclose(got, [o[kk] for kk in KEYS], rtol=1e-9, atol=0), (f, pol, s)
+    assert min(agg.values()) >= 0.9, agg
