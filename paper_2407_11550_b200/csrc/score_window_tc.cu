@@ -22,8 +22,12 @@
 //   MN-major shared tile and the per-head row sums are a second tcgen05 MMA:
 //   D2[key][head] = E^T[key][row] * Hd[row][head] (Hd = head indicator), fp32 accumulate in
 //   TMEM.  Scores = D2 * 2^-16, group score = sum over heads / g.
-// Both passes run back to back per slice of problems small enough (~48 MB of K) to stay
-// L2-resident, so pass 2 re-reads K from L2 (pass 1 loads evict_last, pass 2 evict_first).
+// The two passes run over ALL problems of a call (one pass-1 launch, one pass-2 launch).
+// Slicing the call into L2-sized runs of groups (so pass 2 would re-read K from L2) was
+// measured and dropped: ncu with --cache-control none shows pass 2 reading its whole slice from
+// DRAM even at 42 MB slices (L2 hit rate 28%), and every slice boundary costs a grid tail --
+// 32 layers of config 2 take 62 / 44 / 39 / 30 us per layer at 24 / 48 / 64 MB / unsliced
+// (scripts/score_l2.sh).  ADAKV_SCORE_SLICE_MB still caps a slice for such experiments.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -256,7 +260,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     if (warp == 0) {
         // ===================== TMA producer =====================
         if (lane == 0) {
-            const uint64_t pol = pass2 ? policy_evict_first() : policy_evict_last();
+            const uint64_t pol = policy_evict_first();  // K streams through once per pass (no L2 reuse)
             const uint64_t pol_q = policy_evict_last();
             uint32_t stage = 0, sphase = 0, qphase = 0;
             long long prod_wait = 0;
@@ -614,10 +618,16 @@ namespace {
 
 Plan make_plan(const adakv_layer_shape& s, int pad) {
     Plan pl{};
-    const int64_t k_bytes = s.kv_groups * (s.outside + s.window) * s.head_dim * 2;
-    pl.slice = std::max<int64_t>(1, std::min<int64_t>(s.problems, (48ll << 20) / std::max<int64_t>(k_bytes, 1)));
+    // a slice = a run of KV groups (across problems); default: the whole call (see the header)
+    static const int64_t budget = [] {
+        const char* e = std::getenv("ADAKV_SCORE_SLICE_MB");
+        const int64_t v = e ? std::atoll(e) : 0;
+        return v > 0 ? (v << 20) : (int64_t(1) << 62);
+    }();
+    const int64_t g_bytes = (s.outside + s.window) * s.head_dim * 2;
+    pl.slice = std::max<int64_t>(1, std::min<int64_t>(s.problems * s.kv_groups, budget / std::max<int64_t>(g_bytes, 1)));
     const int sms = device_sm_count();
-    const int64_t pgs = pl.slice * s.kv_groups * std::max(1, vsplit_of(s));
+    const int64_t pgs = pl.slice * std::max(1, vsplit_of(s));
     balance(pgs, ceil_div(s.outside, kTile), sms, &pl.tpi1, &pl.chunks1);
     balance(pgs, ceil_div(s.outside, kTile - 2 * pad), sms, &pl.tpi2, &pl.chunks2);
     return pl;
@@ -644,7 +654,7 @@ bool score_window_tc_supported(adakv_dtype dt, const adakv_layer_shape& s, int64
 size_t score_window_tc_workspace(const adakv_layer_shape& s) {
     const Plan pl = make_plan(s, 0);
     const int64_t vs = std::max(1, vsplit_of(s));
-    const int64_t pgs_slice = pl.slice * s.kv_groups * vs;
+    const int64_t pgs_slice = pl.slice * vs;
     return 3 * 256 + size_t(pgs_slice) * pl.chunks1 * 4 * 128 * 2 * 4 +
            size_t(s.problems * s.kv_groups * vs) * 128 * 2 * 4 + size_t(pgs_slice) * 4;
 }
@@ -658,10 +668,10 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
     const int64_t d = s.head_dim;
     const int64_t vs = vsplit_of(s), Gv = G * vs, gst = gs / vs;  // virtual groups of gst heads
     Arena ar(ws);
-    float* partial = ar.take<float>(size_t(pl.slice * Gv * pl.chunks1 * 4 * 256));
+    float* partial = ar.take<float>(size_t(pl.slice * vs * pl.chunks1 * 4 * 256));
     float* fstats = ar.take<float>(size_t(s.problems * Gv * 256));
-    unsigned* tickets = ar.take<unsigned>(size_t(pl.slice * Gv));
-    ADAKV_CUDA_TRY(cudaMemsetAsync(tickets, 0, size_t(pl.slice * Gv) * 4, stream));
+    unsigned* tickets = ar.take<unsigned>(size_t(pl.slice * vs));
+    ADAKV_CUDA_TRY(cudaMemsetAsync(tickets, 0, size_t(pl.slice * vs) * 4, stream));
     if (vs > 1)  // the virtual groups' halves are added into the group scores
         ADAKV_CUDA_TRY(cudaMemsetAsync(group_scores, 0, size_t(s.problems * G * s.outside) * 4, stream));
     const size_t smem = smem_bytes();
@@ -671,13 +681,13 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
     ADAKV_CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ADAKV_CUDA_TRY(cudaFuncSetAttribute(score_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const float sc = scale ? 1.0f / sqrtf(float(d)) : 1.0f;
-    for (int64_t p0 = 0; p0 < s.problems; p0 += pl.slice) {
-        const int64_t np = std::min(pl.slice, s.problems - p0);
+    for (int64_t g0 = 0; g0 < s.problems * G; g0 += pl.slice) {
+        const int64_t ng = std::min(pl.slice, s.problems * G - g0);  // KV groups of this slice
         CUtensorMap tq, tk;
-        const auto* qb = static_cast<const __nv_bfloat16*>(q) + p0 * H * m * d;
-        const auto* kb = static_cast<const __nv_bfloat16*>(k) + p0 * G * n * d;
-        ADAKV_TRY(make_map(&tq, qb, uint64_t(gst * m), uint64_t(np * Gv)));
-        ADAKV_TRY(make_map(&tk, kb, uint64_t(n), uint64_t(np * G)));
+        const auto* qb = static_cast<const __nv_bfloat16*>(q) + g0 * gs * m * d;
+        const auto* kb = static_cast<const __nv_bfloat16*>(k) + g0 * n * d;
+        ADAKV_TRY(make_map(&tq, qb, uint64_t(gst * m), uint64_t(ng * vs)));
+        ADAKV_TRY(make_map(&tk, kb, uint64_t(n), uint64_t(ng)));
         TcParams prm{};
         prm.G = int(G);
         prm.H = int(H);
@@ -685,7 +695,7 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
         prm.vsplit = int(vs);
         prm.m = int(m);
         prm.n_o = int(s.outside);
-        prm.pg_base = int(p0 * Gv);
+        prm.pg_base = int(g0 * vs);
         prm.scale_log2 = sc * 1.4426950408889634f;
         prm.log2_m = log2f(float(m));
         prm.inv_g = 1.0f / float(gs);
@@ -708,7 +718,7 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
         prm.tiles_per_pg = int(ceil_div(s.outside, kTile));
         prm.tiles_per_item = pl.tpi1;
         prm.chunks_per_pg = pl.chunks1;
-        prm.n_items = int(np * Gv * prm.chunks_per_pg);
+        prm.n_items = int(ng * vs * prm.chunks_per_pg);
         int grid = std::min(prm.n_items, sms);
         cudaLaunchAttribute pdl[1];
         pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -719,7 +729,7 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
         lc.stream = stream;
         lc.attrs = pdl;
         lc.gridDim = dim3(unsigned(grid));
-        lc.numAttrs = p0 > 0 ? 1 : 0;  // the first pass 1 waits for whatever produced K
+        lc.numAttrs = g0 > 0 ? 1 : 0;  // the first pass 1 waits for whatever produced K
         ADAKV_CUDA_TRY(cudaLaunchKernelEx(&lc, score_tc_kernel<0>, tq, tk, prm));
         // pass 2: pooled scores over (128 - 2 pad)-key output tiles
         prm.pass = 2;
@@ -728,7 +738,7 @@ adakv_status score_window_tc(const adakv_layer_shape& s, int64_t pool_kernel, in
         prm.tiles_per_pg = int(ceil_div(s.outside, prm.step));
         prm.tiles_per_item = pl.tpi2;
         prm.chunks_per_pg = pl.chunks2;
-        prm.n_items = int(np * Gv * prm.chunks_per_pg);
+        prm.n_items = int(ng * vs * prm.chunks_per_pg);
         grid = std::min(prm.n_items, sms);
         if (dbg & 1) continue;  // debug: pass 1 only
         lc.gridDim = dim3(unsigned(grid));
