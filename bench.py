@@ -527,7 +527,7 @@ def run_ours(args, cfg):
     dec_launch_us = dm * 1e3 / (S * L)
     dec_bytes_launch = bytes_d / (S * L)
     traffic = {}
-    tf = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    tf = os.path.join(ROOT, "profiles", "r02_traffic.json")
     if os.path.exists(tf):
         with open(tf) as f:
             traffic = json.load(f)
@@ -537,8 +537,10 @@ def run_ours(args, cfg):
                 "achieved": round(dec_bytes_launch / (dec_launch_us * 1e-6) / 1e9, 3), "peak": peak, "unit": "GB/s",
                 "frac": round(dec_bytes_launch / (dec_launch_us * 1e-6) / 1e9 / peak, 4),
                 "traffic": (t["dram_read_bytes"] + t["dram_write_bytes"]) if t else None,
+                "traffic_algorithmic_bytes": t.get("algorithmic_bytes") if t else None,
                 "per_launch_bytes": int(dec_bytes_launch), "avg_launch_us": round(dec_launch_us, 3),
-                "traffic_source": "profiles/r01_traffic.json (ncu, dram bytes per launch)" if t else None}
+                "traffic_source": ("profiles/r02_traffic.json: ncu dram bytes of the step-256 launch (the middle of "
+                                   "the 512 steps) beside that same launch's algorithmic bytes") if t else None}
     else:
         roof = {"kernel": "window scoring (K1)", "bound": "hbm", "achieved": round(score_gbs, 3), "peak": peak,
                 "unit": "GB/s", "frac": round(score_gbs / peak, 4), "traffic": None,
