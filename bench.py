@@ -589,6 +589,7 @@ def run_ours(args, cfg):
         import bench_configs as BC
         line["config3"] = BC.config3(dev, peak, rank, ws)
         line["config4"] = BC.config4(dev, peak, rank, ws)
+        line["config5"] = BC.config5(dev, peak, rank, ws)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         try:

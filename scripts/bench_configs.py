@@ -1,4 +1,4 @@
-"""Supplementary bench lines at BASELINE.json configs 3 and 4 (imported by bench.py).
+"""Supplementary bench lines at BASELINE.json configs 3, 4 and 5 (imported by bench.py).
 
 config 3: Mistral-7B shapes (32 Q / 8 KV heads, d = 128, 32 layers), 128K prompt, batch 8,
           per-head budgets 128 / 1024 / 4096; requests batch-sharded over the ranks (8 / N per
@@ -10,6 +10,9 @@ config 4: Llama-3.1-70B shapes (64 Q / 8 KV heads, 80 layers), 64K prompt, per-h
           (not given in BASELINE.json), batch 1, KV groups sharded over the ranks
           (8 / N groups per rank) with one all-gather per layer (sharding.py); each layer's
           compress is compress_kv_group_sharded, then `steps` decode steps over the 80 layers.
+config 5: Llama-3.1-8B shapes, 32 layers, 32K context, budget 1024/head, question-agnostic
+          (window = the context's last 32 tokens, 64 question tokens appended after
+          compression), 32 requests batch-sharded over the ranks (4 per GPU on 8 GPUs).
 All times are CUDA-event times on the launching stream, max over ranks.
 """
 from __future__ import annotations
@@ -212,3 +215,82 @@ def config4(dev, peak, rank, world, steps=64, reps=2, layers=80):
             "decode_us_per_launch": round(dm * 1e3 / (steps * layers), 3),
             "decode_gbs_per_rank": round(bytes_d_rank / (dm * 1e-3) / 1e9, 1),
             "decode_frac": round(bytes_d_rank / (dm * 1e-3) / 1e9 / peak, 4)}
+
+
+def config5(dev, peak, rank, world, steps=64, reps=2, T=64):
+    """Config 5: question-agnostic compression -- Llama-3.1-8B shapes, 32
+    layers, 32K context, budget 1024/head, 32 requests batch-sharded over the ranks (4 per GPU on
+    8 GPUs).  Per layer the window is the context's last 32 tokens; after compression the T
+    question tokens are appended to every segment (append_rows), then `steps` decode steps."""
+    L, B_all, H, G, d, m, n, budget = 32, 32, 32, 8, 128, 32, 32768, 1024
+    n_o = n - m
+    mine = list(range(rank, B_all, world))
+    B = len(mine)
+    lib = A.lib()
+    inputs = [planted_layer(B, H, G, n_o, m, d, seed=500 + 13 * i + rank, dtype=torch.bfloat16, device=dev)
+              for i in range(2)]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(990 + rank)
+    kq = torch.randn((B * G, T, d), generator=gen, device=dev).to(torch.bfloat16)
+    vq = torch.randn((B * G, T, d), generator=gen, device=dev).to(torch.bfloat16)
+    qs = torch.randn((steps, L, B, H, d), generator=gen, device=dev).to(torch.bfloat16)
+    ks = torch.randn((steps, L, B, G, d), generator=gen, device=dev).to(torch.bfloat16)
+    vs = torch.randn((steps, L, B, G, d), generator=gen, device=dev).to(torch.bfloat16)
+    LB = budget * G
+    reserve = T + steps + 1
+    P = L * B
+    cache = ops.CompressedCache(
+        k=torch.empty((P * (LB + G * reserve), d), dtype=torch.bfloat16, device=dev),
+        v=torch.empty((P * (LB + G * reserve), d), dtype=torch.bfloat16, device=dev),
+        seg_start=torch.empty(P * G, dtype=torch.int32, device=dev),
+        seqlens=torch.empty(P * G, dtype=torch.int32, device=dev),
+        budgets=torch.empty(P * G, dtype=torch.int32, device=dev), P=P, H=H, G=G, m=m, d=d, reserve=reserve,
+        layer_budget=LB, seg_cap=torch.empty(P * G, dtype=torch.int32, device=dev))
+
+    def compress_all():
+        for l in range(L):
+            q, k, v = inputs[l & 1]
+            ops.compress(q, k, v, LB, reserve=reserve, out=cache, first_problem=l * B)
+        # the question tokens after compression: every layer's segments get the same T rows here
+        for l in range(L):
+            sub = ops.CompressedCache(k=cache.k, v=cache.v, seg_start=cache.seg_start[l * B * G:(l + 1) * B * G],
+                                      seqlens=cache.seqlens[l * B * G:(l + 1) * B * G], budgets=cache.budgets,
+                                      P=B, H=H, G=G, m=m, d=d, reserve=reserve, layer_budget=LB,
+                                      seg_cap=cache.seg_cap[l * B * G:(l + 1) * B * G])
+            ops.append_rows(sub, kq, vq, check=False)
+
+    compress_all()
+    seq_q = cache.seqlens.clone()
+    max_rows = int(cache.seg_cap.max())
+    outs = torch.empty((L, B, H, d), dtype=torch.bfloat16, device=dev)
+    dws = torch.zeros(ops.decode_workspace_bytes(B, H, G, d, max_rows), dtype=torch.uint8, device=dev)
+    graph = _decode_graph(lib, lambda l: (cache, l), L, B, qs, ks, vs, outs, dws, max_rows)
+    cms, dms = [], []
+    for _ in range(reps + 1):
+        if dist.is_initialized():
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1, e2 = _ev(), _ev(), _ev()
+        e0.record()
+        compress_all()
+        e1.record()
+        cache.seqlens.copy_(seq_q)
+        graph.replay()
+        e2.record()
+        torch.cuda.synchronize()
+        cms.append(e0.elapsed_time(e1))
+        dms.append(e1.elapsed_time(e2))
+    cm = _max_over_ranks(float(np.median(cms[1:])), dev)
+    dm = _max_over_ranks(float(np.median(dms[1:])), dev)
+    rows0 = int(seq_q.to(torch.int64).sum())
+    bytes_c = world * (PL.algorithmic_bytes_compress(L, B, H, G, n_o, m, d, LB) + L * B * G * T * 2 * 2 * d * 2)
+    rows_total = steps * rows0 + P * G * steps * (steps + 1) // 2
+    bytes_d = world * (2 * 2 * d * rows_total + steps * L * B * (2 * 2 * H * d + 2 * 2 * G * d))
+    return {"workload": f"Llama-3.1-8B shapes, 32 layers, 32K context, budget {budget}/head, question-agnostic "
+                        f"(window = last 32 context tokens, {T} question tokens appended after compression), "
+                        f"32 requests ({B} per rank x {world} ranks), {steps} decode steps",
+            "scaling": "strong (32 requests split over the ranks)",
+            "compress_ms_per_layer": round(cm / L, 4), "compress_gbs": round(bytes_c / (cm * 1e-3) / 1e9, 1),
+            "compress_frac": round(bytes_c / (cm * 1e-3) / 1e9 / peak, 4),
+            "decode_us_per_launch": round(dm * 1e3 / (steps * L), 3),
+            "decode_gbs": round(bytes_d / (dm * 1e-3) / 1e9, 1), "decode_frac": round(bytes_d / (dm * 1e-3) / 1e9 / peak, 4)}
