@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <cmath>
+#include <cstdio>
 #include <string>
 
 #include "adakv_b200.h"
@@ -37,6 +38,23 @@ enum : uint32_t {
     ERR_CAPACITY = 1u << 3,    // decode append beyond reserved capacity
     ERR_MAXROWS = 1u << 4,     // a decode segment longer than the call's max_rows bound
 };
+
+// Device-side bounds assertions (a checked build: make EXTRA=-DADAKV_DEVICE_CHECKS; used in
+// place of compute-sanitizer, which this GPU pool does not allow).  Compiled out otherwise.
+#ifdef ADAKV_DEVICE_CHECKS
+#define ADAKV_DCHECK(cond)                                                                      \
+    do {                                                                                        \
+        if (!(cond)) {                                                                          \
+            printf("ADAKV_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+                   int(blockIdx.x), int(threadIdx.x));                                          \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define ADAKV_DCHECK(cond) \
+    do {                   \
+    } while (0)
+#endif
 
 // ---------------------------------------------------------------- workspace
 // Bump allocator: the same code computes sizes (base == nullptr) and carves.

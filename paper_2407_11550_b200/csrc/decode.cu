@@ -180,6 +180,7 @@ __global__ void append_kernel(int64_t segments, int64_t rows, int64_t d, const i
         return;
     }
     const int64_t row0 = int64_t(seg_start[s]) + seqlens[s];
+    ADAKV_DCHECK(seqlens[s] >= 0 && row0 + rows <= int64_t(seg_start[s]) + seg_cap[s]);
     const int64_t w = d * esz_units;  // row width in 16-bit units
     for (int64_t i = threadIdx.x; i < rows * w; i += blockDim.x) {
         kc[row0 * w + i] = kn[s * rows * w + i];

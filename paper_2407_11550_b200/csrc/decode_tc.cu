@@ -196,6 +196,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     // this layer's own cache state (written by its previous decode step, long complete)
     const int L_old = __ldcg(seqlens + pg);
     const int base = seg_start[pg];
+    ADAKV_DCHECK(L_old >= 0 && base >= 0 && L_old <= seg_cap[pg]);
     // append_kv into a full segment is refused (never written past seg_cap): the step attends
     // the existing rows and ERR_CAPACITY is latched after the dependency wait
     const bool append = k_new != nullptr && L_old < seg_cap[pg];

@@ -116,7 +116,9 @@ gather_kernel(const V* __restrict__ k, const V* __restrict__ v, int64_t G, int64
         while (cum[g + 1] <= r) ++g;
         const int64_t rin = r - cum[g];
         const int64_t b = bcum[g + 1] - bcum[g];
+        ADAKV_DCHECK(g < G && rin >= 0 && (rin >= b || bcum[g] + rin < kept_stride));
         const int64_t src_row = rin < b ? int64_t(kept_pos[p * kept_stride + bcum[g] + rin]) : n_o + (rin - b);
+        ADAKV_DCHECK(src_row >= 0 && src_row < n_rows && (rin >= b ? true : src_row < n_o));
         const int64_t src = ((p * G + g) * n_rows + src_row) * vec_per_row + c;
         const int64_t dst = (int64_t(seg_start[p * G + g]) + rin) * vec_per_row + c;
         const V kx = k[src], vx = v[src];

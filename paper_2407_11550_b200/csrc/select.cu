@@ -634,6 +634,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
             const int pos0 = int(a - off_s);
             auto emit = [&](int j, bool valid, bool keep) {
                 const unsigned bk = __ballot_sync(0xffffffffu, keep);
+                ADAKV_DCHECK(!(keep && kp) || run_kept + __popc(bk & lt) < prm.kept_stride);
                 if (keep && kp) kp[run_kept + __popc(bk & lt)] = int32_t(pos0 + j);
                 if (valid && keep_out) keep_out[a + j] = keep ? 1 : 0;
                 run_kept += __popc(bk);

@@ -16,7 +16,8 @@ L = A.lib()
 if os.environ.get("NOPDL"):
     L.adakv_set_decode_overlap(0)
 dev = torch.device("cuda:0")
-Lyr, H, G, d, LB = int(os.environ.get("LAYERS", "32")), 32, 8, 128, 16384
+Lyr, H, G, d = int(os.environ.get("LAYERS", "32")), 32, 8, 128
+LB = int(os.environ.get("LBH", "2048")) * G
 B = int(os.environ.get("BATCH", "1"))
 steps = int(os.environ.get("STEPS", "4"))
 reserve = steps + 8
