@@ -360,6 +360,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     if (qmode >= 1) {
         // every warp waits (also those without blocks: no multicast may land in an exited CTA)
         mbar_wait(&S.qbar, 0);
+        if (dbg && warp == 1 && lane == 0) dbg[blockIdx.x * 32 + 14] = clock64();  // (debug) Q landed
         const uint32_t qrow = smem_u32(S.qs) + uint32_t((head_ok ? gid : 0) * d * 2);
 #pragma unroll
         for (int i = 0; i < 4; ++i) qv[i] = lds128(qrow + 16u * uint32_t(i * 4 + tig));
@@ -661,7 +662,7 @@ static DecodeKernel kernel_for_impl(int64_t cs, std::integer_sequence<int, CS...
 }
 static DecodeKernel kernel_for(int64_t cs) { return kernel_for_impl(cs, std::make_integer_sequence<int, kMaxCS>{}); }
 
-// TMA ring depth per warp (ADAKV_DECODE_SLOTS overrides; 1..kMaxSlots)
+// TMA ring depth per warp (ADAKV_DECODE_SLOTS overrides; 2..kMaxSlots)
 static int decode_slots() {
     static int n = [] {
         const char* e = std::getenv("ADAKV_DECODE_SLOTS");
@@ -669,7 +670,8 @@ static int decode_slots() {
         int mx = kMaxSlots;
         while (mx > 1 && dec_smem_bytes(mx, kWarpsDec) > 227 * 1024) --mx;
         const int v = e ? std::atoi(e) : mx;
-        return v < 1 ? 1 : v > mx ? mx : v;
+        // >= 2: a warp takes its blocks two at a time, and both must be in flight at once
+        return v < 2 ? 2 : v > mx ? mx : v;
     }();
     return n;
 }
@@ -726,6 +728,8 @@ int64_t decode_tc_cluster(int64_t P, int64_t G) {
     // the next layer's launch starts, and prefetches, while this one runs: config 2 measures
     // 4.11 us per step-layer at 9 against 4.13 at 10.  Smaller still costs more in per-CTA
     // work than the earlier start saves.
+    if (std::getenv("ADAKV_DEBUG_FIT"))
+        for (int64_t cs = 2; cs <= kMaxCS; ++cs) std::fprintf(stderr, "decode cluster fit cs=%lld: %lld\n", (long long)cs, (long long)fit[cs]);
     int64_t best = 1;
     for (int64_t cs = kMaxCS; cs >= 2 && best == 1; --cs)
         if (fit[cs] >= segs) best = cs;

@@ -134,4 +134,5 @@ ok = w1[:, 4] > 0
 if ok.sum() == 0:
     sys.exit(0)
 r = (w1[ok] - pw[ok][:, None])
-print("warp1 (CTAs with >=2 blocks):", ok.sum(), "med cycles after post_wait: top0 %d data0 %d S0 %d end0 %d top1 %d data1 %d S1 %d end1 %d" % tuple(np.median(r, axis=0)))
+print("warp1 (CTAs with >=2 blocks):", ok.sum(), "med cycles after post_wait: top0 %d data0 %d S0 %d end0 %d top1 %d data1 %d Qlanded %d end1 %d" % tuple(np.median(r, axis=0)))
+print("  p90: top0 %d data0 %d S0 %d end0 %d top1 %d data1 %d Qlanded %d end1 %d" % tuple(np.percentile(r, 90, axis=0)))
