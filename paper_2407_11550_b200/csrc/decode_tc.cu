@@ -189,8 +189,8 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
         if (dbg && threadIdx.x == 0) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-            dbg[blockIdx.x * 32 + k] = t;
-            if (k < 8) dbg[blockIdx.x * 32 + 16 + k] = clock64();
+            dbg[blockIdx.x * 64 + k] = t;
+            if (k < 8) dbg[blockIdx.x * 64 + 16 + k] = clock64();
         }
     };
     // this layer's own cache state (written by its previous decode step, long complete)
@@ -305,7 +305,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     if (append && nb > 0 && (w_hi * kBlk > L_old))
         new_chunk = reinterpret_cast<const uint4*>((lane < 16 ? k_new : v_new) + int64_t(pg) * d)[lane & 15];
     auto wstamp = [&](int j, int k) {  // (debug) warp 1's first two blocks: cycles per phase
-        if (dbg && warp == 1 && lane == 0 && j < 2) dbg[blockIdx.x * 32 + 8 + 4 * j + k] = clock64();
+        if (dbg && warp == 1 && lane == 0 && j < 2) dbg[blockIdx.x * 64 + 8 + 4 * j + k] = clock64();
     };
     int s = 0;
     uint32_t sphase = 0;  // slot and mbarrier phase of block j (no division in the loop)
@@ -360,7 +360,8 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     if (qmode >= 1) {
         // every warp waits (also those without blocks: no multicast may land in an exited CTA)
         mbar_wait(&S.qbar, 0);
-        if (dbg && warp == 1 && lane == 0) dbg[blockIdx.x * 32 + 14] = clock64();  // (debug) Q landed
+        if (dbg && warp == 1 && lane == 0) dbg[blockIdx.x * 64 + 14] = clock64();  // (debug) Q landed
+        if (dbg && lane == 0) dbg[blockIdx.x * 64 + 32 + 4 * warp] = clock64();
         const uint32_t qrow = smem_u32(S.qs) + uint32_t((head_ok ? gid : 0) * d * 2);
 #pragma unroll
         for (int i = 0; i < 4; ++i) qv[i] = lds128(qrow + 16u * uint32_t(i * 4 + tig));
@@ -494,6 +495,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             scores(j, kva, *reinterpret_cast<float(*)[4]>(&x[0]));
             scores(j + 1, kvb, *reinterpret_cast<float(*)[4]>(&x[4]));
             wstamp(j, 2);
+            if (dbg && lane == 0 && j == 0) dbg[blockIdx.x * 64 + 33 + 4 * warp] = clock64();
             softmax(x, 8);
             uint4 vv[4][2];
             load_v(s, vv);
@@ -504,6 +506,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
             if (lane == 0 && j + nslots < nb) issue(j + nslots);
             if (lane == 0 && j + 1 + nslots < nb) issue(j + 1 + nslots);
             wstamp(j, 3);
+            if (dbg && lane == 0 && j == 0) dbg[blockIdx.x * 64 + 34 + 4 * warp] = clock64();
             s = s1;
             sphase = ph1;
             advance(s, sphase);
@@ -526,7 +529,8 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     if (dbg && lane == 0 && warp < 8) {  // (debug) every warp's loop end + its block count
         unsigned long long t;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-        dbg[blockIdx.x * 32 + 24 + warp] = t;
+        dbg[blockIdx.x * 64 + 24 + warp] = t;
+        dbg[blockIdx.x * 64 + 35 + 4 * warp] = clock64();
     }
     // ---- (1) warp partial -> smem: (m, l) per head; O into the warp's idle ring in a skewed
     // [column][8 heads] layout (8 words of padding per 8 columns, so the lanes' float2 (ha, hb)

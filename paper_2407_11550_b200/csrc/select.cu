@@ -137,8 +137,12 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
 
     int nst = 0;
     auto stamp = [&]() {
-        if (dbg && tid == 0 && nst < 32) dbg[blockIdx.x * 32 + nst] = clock64();
+        if (dbg && tid == 0 && nst < 24) dbg[blockIdx.x * 32 + nst] = clock64();
         ++nst;
+    };
+    int fine_pass = -1;  // (debug) fine stamps of one radix pass into slots 24..31
+    auto fstamp = [&](int k) {
+        if (dbg && tid == 0 && fine_pass == 1) dbg[blockIdx.x * 32 + 24 + k] = clock64();
     };
     stamp();
     if (tid == 0) {
@@ -257,6 +261,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     // histograms of elements matching that segment's prefix, cluster-summed into agg.
     int buf = 0;  // histogram double buffer; toggled only by a pass that used it
     auto radix_pass = [&](int pass) {
+        fine_pass = pass;
+        fstamp(0);
         const int shift = lo_bit(pass);
         const KT mask = hi_mask(pass);
         uint32_t* hb = hist + buf * S * 256;
@@ -301,7 +307,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                     if (key >= 0) atomicAdd(&my[key], 1u);  // warp-private: only intra-warp collisions
                 }
             }
+            fstamp(1);
             __syncthreads();
+            fstamp(2);
             if (tid < 256) {
                 uint32_t t = 0;
 #pragma unroll 8
@@ -309,8 +317,10 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                 hb[s * 256 + tid] = t;
             }
             __syncthreads();
+            fstamp(3);
         }
         cluster.sync();
+        fstamp(4);
         // sum the CS histograms through DSMEM: all remote loads issued before any is used
         // (segment s has elements only in ranks [r0, r1]: the others' histograms are zero)
         for (int i0 = tid; i0 < S * 256; i0 += 2 * kSelThreads) {
@@ -332,7 +342,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                     agg[i] = ((v[u][0] + v[u][1]) + (v[u][2] + v[u][3])) + ((v[u][4] + v[u][5]) + (v[u][6] + v[u][7]));
             }
         }
+        fstamp(5);
         __syncthreads();
+        fstamp(6);
         buf ^= 1;
         stamp();
     };
@@ -691,6 +703,7 @@ adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStre
     const int64_t per_cta = 16384;
     int CS = int(ceil_div(prm.N, per_cta));
     CS = CS < 1 ? 1 : (CS > 8 ? 8 : CS);
+    if (const char* e = std::getenv("ADAKV_SELECT_CS")) CS = std::max(1, std::min(8, std::atoi(e)));
     size_t smem = select_smem_bytes(prm.S);
     const size_t key_bytes = size_t(ceil_div(prm.N, CS)) * (key64 ? 8 : 4) + 16;  // + vector-read slack
     SelParams lp = prm;

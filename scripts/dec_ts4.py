@@ -40,7 +40,7 @@ cache = CompressedCache(k=kp, v=vp, seg_start=torch.as_tensor(starts, device=dev
 dg = PL.DecodeGraph(cache, Lyr, B, int(caps.max()), use_graph=False)
 dg.q.normal_()
 nl = steps * Lyr
-dbg = torch.zeros((nl, 256, 32), dtype=torch.int64, device=dev)
+dbg = torch.zeros((nl, 256, 64), dtype=torch.int64, device=dev)
 st = torch.cuda.Stream()
 st.wait_stream(torch.cuda.current_stream())
 g = torch.cuda.CUDAGraph()
@@ -136,3 +136,11 @@ if ok.sum() == 0:
 r = (w1[ok] - pw[ok][:, None])
 print("warp1 (CTAs with >=2 blocks):", ok.sum(), "med cycles after post_wait: top0 %d data0 %d S0 %d end0 %d top1 %d data1 %d Qlanded %d end1 %d" % tuple(np.median(r, axis=0)))
 print("  p90: top0 %d data0 %d S0 %d end0 %d top1 %d data1 %d Qlanded %d end1 %d" % tuple(np.percentile(r, 90, axis=0)))
+pw4 = half[:, :, 18][act]
+ww = half[:, :, 32:64][act].reshape(-1, 8, 4)
+okw = ww[:, :, 1] > 0
+print("per-warp cycles after post_wait (median over CTAs/launches): Q landed | first pair S done | first pair PV done | loop end")
+for w in range(8):
+    sel = okw[:, w]
+    r = ww[sel, w, :] - pw4[sel][:, None]
+    print(f"  warp {w}: " + " ".join(f"{int(np.median(r[:, k])):6d}" for k in range(4)), f"(n={sel.sum()})")

@@ -26,7 +26,12 @@ L.adakv_debug_set_select_timestamps(None)
 x = dbg.cpu().numpy()
 act = x[:, 0] > 0
 rel = x[act] - x[act][:, :1]
-n_st = int((x[act] > 0).sum(axis=1).max())
+n_st = int((x[act][:, :24] > 0).sum(axis=1).max())
 print("CTAs", int(act.sum()), "stamps", n_st)
 print("median cycles since start:", [int(np.median(rel[:, i])) for i in range(n_st)])
 print("max    cycles since start:", [int(np.max(rel[:, i])) for i in range(n_st)])
+fine = x[act][:, 24:31]
+if (fine > 0).all():
+    d = np.diff(fine, axis=1)
+    print("radix pass 1 phases (key loop, sync, warp-sum+sync, cluster.sync, DSMEM sum, sync):",
+          [int(np.median(d[:, i])) for i in range(d.shape[1])])
