@@ -297,6 +297,7 @@ def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
     import paper_2407_11550_b200 as A
+    from paper_2407_11550_b200 import ops
     from paper_2407_11550_b200 import pipeline as PL
     from paper_2407_11550_b200.synthetic import planted_layer
 
@@ -458,6 +459,12 @@ def run_ours(args, cfg):
             probe.append((tag, e))
 
     compressed_ev = torch.cuda.Event()
+    # each chunk's gather (reading V's retained rows over the host link) is forked onto a
+    # gather stream so it overlaps the next chunk's scoring; two chunk workspaces alternate
+    gather_st = torch.cuda.Stream(device=dev)
+    cws_n = ops.compress_workspace_bytes(q[:lc].reshape(lc * B, *q.shape[2:]), k[:lc].reshape(lc * B, *k.shape[2:]))
+    cws = [torch.zeros(cws_n, dtype=torch.uint8, device=dev) for _ in range(2)]
+    gathered = [torch.cuda.Event(), torch.cuda.Event()]
 
     def h2d_into(i, after=None):
         with torch.cuda.stream(copy_st):
@@ -484,8 +491,13 @@ def run_ours(args, cfg):
             mark(f"req{r}", comp_st)
             for c in range(nch):
                 comp_st.wait_event(chunk_in[i][c])
+                if c >= 2:
+                    comp_st.wait_event(gathered[c & 1])  # chunk c-2's gather is done with this workspace
                 sl = slice(c * lc, (c + 1) * lc)
-                PL.compress_model(qi[sl], ki[sl], vh[sl], LB, reserve=reserve, out=cache, first_layer=c * lc)
+                PL.compress_model(qi[sl], ki[sl], vh[sl], LB, reserve=reserve, out=cache, first_layer=c * lc,
+                                  ws=cws[c & 1], gather_stream=gather_st)
+                gathered[c & 1].record(gather_st)
+            comp_st.wait_stream(gather_st)  # join: the whole cache is written
             mark("compressed", comp_st)
             # the next request's copies start once this one's compress (whose gather reads the
             # retained V rows over the same host link) is done; they still land long before this
@@ -505,7 +517,9 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
-    ne2e = max(2, args.steps)
+    # a stream of requests: the first request's prompt copy (the pipeline fill, ~45 ms) is
+    # inside the timed region and amortised over the stream as in serving
+    ne2e = max(args.e2e_requests, args.steps)
     t0.record(comp_st)
     copy_st.wait_event(t0)
     e2e_run(ne2e)
@@ -572,8 +586,10 @@ def run_ours(args, cfg):
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms, 3), "requests": ne2e,
                 "overlap": "next request's Q/K/decode-input H2D on a copy stream during the current decode "
                            "(started after the current compress, whose gather reads V's retained rows over the same "
-                           "link); layers compressed in 4 chunks as they land; V read in place from pinned host "
-                           "memory (retained + window rows only, counted in h2d_bytes_per_step)"},
+                           "link); layers compressed in 4 chunks as they land, each chunk's gather forked onto a "
+                           "second stream (adakv_compress_split) so it overlaps the next chunk's scoring; V read in "
+                           "place from pinned host memory (retained + window rows only, counted in "
+                           "h2d_bytes_per_step); the first request's copy (pipeline fill) is inside the timed region"},
         "peak_source": src,
     }
     if scal:
@@ -623,6 +639,8 @@ def main():
     ap.add_argument("--decode-steps", type=int)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the config3 / config4 fields")
+    ap.add_argument("--e2e-requests", type=int, default=16,
+                    help="requests streamed through the e2e leg (at least --steps)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
         return relaunch(args)

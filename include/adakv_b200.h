@@ -158,6 +158,25 @@ adakv_status adakv_compress(adakv_dtype dtype, const adakv_layer_shape* shape,
                             int32_t* seg_start, int32_t* seqlens, int32_t* seg_cap, int32_t* budgets,
                             void* group_scores, uint8_t* keep, void* workspace,
                             size_t workspace_bytes, adakv_stream_t stream);
+/* adakv_compress with the final gather (the copy of the retained K/V rows into the cache
+ * planes) enqueued on `gather_stream` instead of `stream`, after an event recorded on
+ * `stream` once the selection and the layout are written; `stream` does not wait for it.
+ * For a model compressed in layer chunks as its prompt arrives, chunk i's gather -- bound by
+ * the host link when V is in pinned host memory -- then overlaps chunk i+1's scoring.  The
+ * gather reads this call's workspace (kept positions) and writes its error word, so:
+ *   - k_cache / v_cache (and the workspace status) are complete only once the caller has
+ *     made its next reader wait for gather_stream (cudaStreamWaitEvent);
+ *   - the workspace must not be reused on `stream` before that wait.
+ * gather_stream == NULL or == stream is adakv_compress exactly.  (No reference counterpart:
+ * evict_layer is one synchronous call, policies.hpp:204-293.) */
+adakv_status adakv_compress_split(adakv_dtype dtype, const adakv_layer_shape* shape,
+                                  const adakv_policy_config* cfg, int64_t layer_budget,
+                                  const int64_t* layer_budgets, const void* q, const void* k,
+                                  const void* v, int64_t reserve, void* k_cache, void* v_cache,
+                                  int32_t* seg_start, int32_t* seqlens, int32_t* seg_cap,
+                                  int32_t* budgets, void* group_scores, uint8_t* keep, void* workspace,
+                                  size_t workspace_bytes, adakv_stream_t stream,
+                                  adakv_stream_t gather_stream);
 adakv_status adakv_compress_workspace(adakv_dtype dtype, const adakv_layer_shape* shape,
                                       const adakv_policy_config* cfg, size_t* bytes);
 /* Rows of each output plane: P * (layer_budget + G * reserve), or the sum over

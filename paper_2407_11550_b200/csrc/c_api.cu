@@ -411,12 +411,12 @@ adakv_status adakv_compress_workspace(adakv_dtype dtype, const adakv_layer_shape
     return ADAKV_OK;
 }
 
-adakv_status adakv_compress(adakv_dtype dtype, const adakv_layer_shape* shape, const adakv_policy_config* cfg,
-                            int64_t layer_budget, const int64_t* layer_budgets, const void* q,
-                            const void* k, const void* v, int64_t reserve, void* k_cache, void* v_cache,
-                            int32_t* seg_start, int32_t* seqlens, int32_t* seg_cap, int32_t* budgets,
-                            void* group_scores,
-                            uint8_t* keep, void* workspace, size_t workspace_bytes, adakv_stream_t stream) {
+static adakv_status compress_impl(adakv_dtype dtype, const adakv_layer_shape* shape, const adakv_policy_config* cfg,
+                                  int64_t layer_budget, const int64_t* layer_budgets, const void* q, const void* k,
+                                  const void* v, int64_t reserve, void* k_cache, void* v_cache, int32_t* seg_start,
+                                  int32_t* seqlens, int32_t* seg_cap, int32_t* budgets, void* group_scores,
+                                  uint8_t* keep, void* workspace, size_t workspace_bytes, adakv_stream_t stream,
+                                  adakv_stream_t gather_stream) {
     ADAKV_TRY(validate_dtype(dtype));
     ADAKV_TRY(validate_config(cfg));
     ADAKV_TRY(validate_shape(shape));
@@ -477,8 +477,40 @@ adakv_status adakv_compress(adakv_dtype dtype, const adakv_layer_shape* shape, c
     ADAKV_TRY(launch_layout(budgets, s.problems, G, m, reserve, layer_budget, layer_budgets, seg_start,
                             seqlens, seg_cap, st));
     const int64_t max_rows = layer_budgets ? G * (n_o + m) : layer_budget;
+    cudaStream_t gst = st;
+    if (gather_stream && reinterpret_cast<cudaStream_t>(gather_stream) != st) {
+        // fork: the gather waits for the layout on `stream`, which itself goes on
+        gst = reinterpret_cast<cudaStream_t>(gather_stream);
+        cudaEvent_t ev;
+        ADAKV_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        cudaError_t e = cudaEventRecord(ev, st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(gst, ev, 0);
+        cudaEventDestroy(ev);  // released once the wait has been satisfied
+        ADAKV_CUDA_TRY(e);
+    }
     return launch_gather(dtype, s, max_rows, k, v, budgets, L.kept_pos, L.kept_stride, seg_start, k_cache,
-                         v_cache, L.err, st);
+                         v_cache, L.err, gst);
+}
+
+adakv_status adakv_compress(adakv_dtype dtype, const adakv_layer_shape* shape, const adakv_policy_config* cfg,
+                            int64_t layer_budget, const int64_t* layer_budgets, const void* q,
+                            const void* k, const void* v, int64_t reserve, void* k_cache, void* v_cache,
+                            int32_t* seg_start, int32_t* seqlens, int32_t* seg_cap, int32_t* budgets,
+                            void* group_scores,
+                            uint8_t* keep, void* workspace, size_t workspace_bytes, adakv_stream_t stream) {
+    return compress_impl(dtype, shape, cfg, layer_budget, layer_budgets, q, k, v, reserve, k_cache, v_cache, seg_start,
+                         seqlens, seg_cap, budgets, group_scores, keep, workspace, workspace_bytes, stream, nullptr);
+}
+
+adakv_status adakv_compress_split(adakv_dtype dtype, const adakv_layer_shape* shape, const adakv_policy_config* cfg,
+                                  int64_t layer_budget, const int64_t* layer_budgets, const void* q, const void* k,
+                                  const void* v, int64_t reserve, void* k_cache, void* v_cache, int32_t* seg_start,
+                                  int32_t* seqlens, int32_t* seg_cap, int32_t* budgets, void* group_scores,
+                                  uint8_t* keep, void* workspace, size_t workspace_bytes, adakv_stream_t stream,
+                                  adakv_stream_t gather_stream) {
+    return compress_impl(dtype, shape, cfg, layer_budget, layer_budgets, q, k, v, reserve, k_cache, v_cache, seg_start,
+                         seqlens, seg_cap, budgets, group_scores, keep, workspace, workspace_bytes, stream,
+                         gather_stream);
 }
 
 // ------------------------------------------------------------------ decode

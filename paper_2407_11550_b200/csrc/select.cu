@@ -174,8 +174,41 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     // Every pass below re-reads this CTA's slice of keys: read the scores from global memory
     // once, in coalesced order, and keep the order-preserving keys in shared memory.
     const bool cached = prm.cache_keys != 0;
-    if (cached)
-        for (int64_t e = lo + tid; e < hi; e += kSelThreads) kc[e - lo] = KeyOf<F>::get(sc[e]);
+    if (cached) {
+        // 16-byte loads, four in flight per thread (scalar head up to the first aligned element)
+        constexpr int V = 16 / int(sizeof(F));
+        const F* src = sc + lo;
+        const int64_t len = hi - lo;
+        const int64_t mis = int64_t(reinterpret_cast<uintptr_t>(src) / sizeof(F)) % V;
+        const int64_t h0 = min(len, (V - mis) % V);
+        for (int64_t i = tid; i < h0; i += kSelThreads) kc[i] = KeyOf<F>::get(src[i]);
+        const int64_t nv = (len - h0) / V;
+        const uint4* vs = reinterpret_cast<const uint4*>(src + h0);
+        for (int64_t t0 = tid; t0 < nv; t0 += 4 * kSelThreads) {
+            uint4 r[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t t = t0 + int64_t(u) * kSelThreads;
+                r[u] = t < nv ? __ldcs(vs + t) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t t = t0 + int64_t(u) * kSelThreads;
+                if (t >= nv) break;
+                const F* f = reinterpret_cast<const F*>(&r[u]);
+                KT kk[V];
+#pragma unroll
+                for (int c = 0; c < V; ++c) kk[c] = KeyOf<F>::get(f[c]);
+                if (h0 == 0) {
+                    *reinterpret_cast<uint4*>(kc + t * V) = *reinterpret_cast<const uint4*>(kk);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < V; ++c) kc[h0 + t * V + c] = kk[c];
+                }
+            }
+        }
+        for (int64_t i = h0 + nv * V + tid; i < len; i += kSelThreads) kc[i] = KeyOf<F>::get(src[i]);
+    }
     auto key_at = [&](int64_t e) -> KT { return cached ? kc[e - lo] : KeyOf<F>::get(sc[e]); };
     __syncthreads();
     stamp();
@@ -414,35 +447,48 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     __syncthreads();
 
     stamp();
-    // ---------------- Phase C: allocation (one thread, redundantly per CTA, bit-exact fp64)
-    if (tid == 0) {
+    // ---------------- Phase C: allocation (one warp, redundantly per CTA, bit-exact fp64)
+    if (warp == 0) {
         uint32_t e = 0;
         // a per-problem total outside [0, N] (layer budget below the window floor or above the
         // capacity, policies.hpp:229-231, budget.hpp:48-59) is rejected, never selected from
         if (prm.alloc_mode != ADAKV_ALLOC_GIVEN && (g_k < 0 || g_k > N)) e |= ERR_BUDGET;
         const uint64_t k = e ? 0 : uint64_t(g_k);
-        for (int s = 0; s < S; ++s) b_fin[s] = 0;
+        for (int s = lane; s < S; s += 32) b_fin[s] = 0;
+        __syncwarp();
         if (e) {
         } else if (adaptive) {
-            if (prm.blend) e |= safeguard_dev(b_raw, k, S, prm.alpha, b_caps, quotas, b_fin);
+            if (prm.blend) e |= safeguard_warp(b_raw, k, S, prm.alpha, b_caps, quotas, b_fin, lane);
             else
-                for (int s = 0; s < S; ++s) b_fin[s] = b_raw[s];
+                for (int s = lane; s < S; s += 32) b_fin[s] = b_raw[s];
         } else if (prm.alloc_mode == ADAKV_ALLOC_UNIFORM) {
-            e |= uniform_dev(k, S, b_caps, quotas, b_fin);
+            e |= uniform_warp(k, S, b_caps, quotas, b_fin, lane);
         } else {
-            for (int s = 0; s < S; ++s) {
+            bool bad = false;
+            for (int s = lane; s < S; s += 32) {
                 const int64_t b = prm.budgets[p * S + s];
-                if (b < 0 || uint64_t(b) > b_caps[s]) e |= ERR_BUDGET;
+                if (b < 0 || uint64_t(b) > b_caps[s]) bad = true;
                 b_fin[s] = b < 0 ? 0 : (uint64_t(b) > b_caps[s] ? b_caps[s] : uint64_t(b));
             }
+            if (__any_sync(0xffffffffu, bad)) e |= ERR_BUDGET;
         }
-        if (!e && prm.repair) e |= repair_dev(b_fin, b_caps, S);
+        __syncwarp();
+        // repair_zero_budgets only changes anything when a budget is zero
+        if (!e && prm.repair) {
+            bool zero = false;
+            for (int s = lane; s < S; s += 32) zero |= b_fin[s] == 0;
+            if (__any_sync(0xffffffffu, zero)) {
+                uint32_t r = 0;
+                if (lane == 0) r = repair_dev(b_fin, b_caps, S);
+                e |= __shfl_sync(0xffffffffu, r, 0);
+                __syncwarp();
+            }
+        }
         // on any error every budget is zero: the layout and gather after this kernel then copy
         // the window rows only and never index kept positions that were not written
-        if (e)
-            for (int s = 0; s < S; ++s) b_fin[s] = 0;
-        any_active = 0;
-        for (int s = 0; s < S; ++s) {
+        bool act = false;
+        for (int s = lane; s < S; s += 32) {
+            if (e) b_fin[s] = 0;
             const int64_t b = int64_t(b_fin[s]), n = int64_t(b_caps[s]);
             seg_active[s] = 0;
             if (e) {
@@ -464,11 +510,15 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                 seg_active[s] = 1;
                 seg_prefix[s] = common;
                 seg_krem[s] = b;
-                any_active = 1;
+                act = true;
             }
         }
-        s_err = e;
-        if (e && rank == 0) atomicOr(prm.err, e);
+        act = __any_sync(0xffffffffu, act);
+        if (lane == 0) {
+            any_active = act ? 1 : 0;
+            s_err = e;
+            if (e && rank == 0) atomicOr(prm.err, e);
+        }
     }
     __syncthreads();
     if (rank == 0) {

@@ -133,7 +133,8 @@ def host_device_pointer(t: torch.Tensor) -> C.c_void_p:
 def compress(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layer_budget: int, kind="ada_snapkv",
              pool_kernel=7, alpha=0.2, sink_tokens=4, scale=True, reserve=0, layer_budgets=None,
              return_scores=False, return_keep=False, out: CompressedCache | None = None,
-             ws: torch.Tensor | None = None, first_problem: int = 0, validate=False, check=False) -> CompressedCache:
+             ws: torch.Tensor | None = None, first_problem: int = 0, validate=False, check=False,
+             gather_stream: torch.cuda.Stream | None = None) -> CompressedCache:
     """evict_layer (policies.hpp:204-293) for P problems at once.
 
     q [P, H, m, d]; k, v [P, G, n, d] with the observation window in the last m rows.
@@ -149,6 +150,11 @@ def compress(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layer_budget: in
     non-finite entries that reach the window statistics or the copied rows.
     check: synchronise and raise the reference's exception for anything the device latched
     (non-finite input, per-problem budget below the floor / above the capacity).
+    gather_stream: run the final gather (the copy of the retained rows into out.k / out.v) on
+    this stream, forked after the selection (adakv_compress_split): the current stream goes on
+    at once, so a model compressed in chunks overlaps chunk i's gather with chunk i+1's scoring.
+    The caller must make the cache's readers wait for gather_stream, and must not reuse `ws`
+    on the current stream before that (the gather reads it).
     """
     _need_cuda(q, k)
     if v.is_cuda:
@@ -205,13 +211,22 @@ def compress(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layer_budget: in
     L.check(lib.adakv_compress_workspace(dt, C.byref(shape), C.byref(cfg), C.byref(nbytes)))
     if ws is None:
         ws = workspace(nbytes.value, dev, "compress")
-    L.check(lib.adakv_compress(dt, C.byref(shape), C.byref(cfg), int(layer_budget), _p(layer_budgets), _p(q),
-                               _p(k), v_ptr, int(reserve), at(out.k, row0 * d), at(out.v, row0 * d),
-                               at(out.seg_start, p0 * G), at(out.seqlens, p0 * G), at(out.seg_cap, p0 * G),
-                               at(out.budgets, p0 * G), at(out.scores, p0 * G * n_o), at(out.keep, p0 * G * n_o),
-                               _p(ws), ws.numel(), _stream()))
+    args = (dt, C.byref(shape), C.byref(cfg), int(layer_budget), _p(layer_budgets), _p(q), _p(k), v_ptr, int(reserve),
+            at(out.k, row0 * d), at(out.v, row0 * d), at(out.seg_start, p0 * G), at(out.seqlens, p0 * G),
+            at(out.seg_cap, p0 * G), at(out.budgets, p0 * G), at(out.scores, p0 * G * n_o), at(out.keep, p0 * G * n_o),
+            _p(ws), ws.numel(), _stream())
+    if gather_stream is not None:
+        if check:
+            raise L.InvalidArgument(1, "compress: check needs the gather on the current stream")
+        L.check(lib.adakv_compress_split(*args, C.c_void_p(gather_stream.cuda_stream)))
+    else:
+        L.check(lib.adakv_compress(*args))
     if row0:  # the library laid the segments out from row 0 of the planes it was given
-        out.seg_start[p0 * G:(p0 + P) * G] += row0
+        if gather_stream is not None:  # after the forked gather has read them
+            with torch.cuda.stream(gather_stream):
+                out.seg_start[p0 * G:(p0 + P) * G] += row0
+        else:
+            out.seg_start[p0 * G:(p0 + P) * G] += row0
     out._max_rows = None  # capacities were rewritten
     if validate:
         validate_finite(k, ws)
@@ -219,6 +234,19 @@ def compress(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layer_budget: in
     if check:
         workspace_status(ws)
     return out
+
+
+def compress_workspace_bytes(q: torch.Tensor, k: torch.Tensor, kind="ada_snapkv", pool_kernel=7, alpha=0.2,
+                             sink_tokens=4, scale=True) -> int:
+    """Workspace bytes of one compress call on inputs shaped like q [P, H, m, d], k [P, G, n, d]
+    (e.g. to give each in-flight chunk of a split-gather pipeline its own workspace)."""
+    P, H, m, d = q.shape
+    G, n = k.shape[1], k.shape[2]
+    shape = layer_shape(P, H, G, m, n - m, d)
+    cfg = policy_config(kind, pool_kernel, alpha, sink_tokens, H // G if G else 1, scale, m)
+    nbytes = C.c_size_t()
+    L.check(L.lib().adakv_compress_workspace(_dt(q), C.byref(shape), C.byref(cfg), C.byref(nbytes)))
+    return nbytes.value
 
 
 def validate_finite(x: torch.Tensor, ws: torch.Tensor) -> None:

@@ -20,18 +20,20 @@ from . import ops
 
 
 def compress_model(q, k, v, layer_budget, *, kind="ada_snapkv", pool_kernel=7, alpha=0.2, sink_tokens=4,
-                   reserve=0, layer_budgets=None, out=None, ws=None, first_layer=0) -> ops.CompressedCache:
+                   reserve=0, layer_budgets=None, out=None, ws=None, first_layer=0,
+                   gather_stream=None) -> ops.CompressedCache:
     """q [L, B, H, m, d]; k, v [L, B, G, n, d] -> one CompressedCache with P = L*B problems.
 
     first_layer: with `out` (a cache over the whole model), these L layers are the model's
-    layers [first_layer, first_layer + L) -- layers compressed in chunks as they arrive."""
+    layers [first_layer, first_layer + L) -- layers compressed in chunks as they arrive.
+    gather_stream: see ops.compress (the chunk's gather forked onto that stream)."""
     Lyr, B = q.shape[:2]
     qq = q.reshape(Lyr * B, *q.shape[2:])
     kk = k.reshape(Lyr * B, *k.shape[2:])
     vv = v.reshape(Lyr * B, *v.shape[2:])
     return ops.compress(qq, kk, vv, layer_budget, kind=kind, pool_kernel=pool_kernel, alpha=alpha,
                         sink_tokens=sink_tokens, reserve=reserve, layer_budgets=layer_budgets, out=out, ws=ws,
-                        first_problem=first_layer * B)
+                        first_problem=first_layer * B, gather_stream=gather_stream)
 
 
 def pyramid_problem_budgets(avg_outside_per_layer, layers, batch, G, m, beta_max=1.5, beta_min=0.5, device=None):

@@ -168,3 +168,45 @@ def test_decode_workspace_reuse_across_layouts(dev, oracle_mod):
             ref = O.decode_attention(qd[p].cpu().numpy(), torch.cat([s[0] for s in segs]).cpu().numpy(),
                                      torch.cat([s[1] for s in segs]).cpu().numpy(), off)
             assert np.allclose(o[p].cpu().numpy(), ref, rtol=1e-10, atol=1e-12), (P, p)
+
+
+@pytest.mark.parametrize("host_v", [False, True])
+def test_compress_split_gather_chunks_match_one_call(dev, host_v):
+    """adakv_compress_split: a model compressed in layer chunks with every chunk's gather forked
+    onto a second stream (two alternating workspaces, joined before use) -- with V on the device
+    or in pinned host memory -- writes exactly the cache one adakv_compress call writes."""
+    from paper_2407_11550_b200 import pipeline as PL
+    Lyr, B, H, G, m, n, d = 8, 1, 32, 8, 32, 1056, 128
+    q, k, v = planted_layer(Lyr * B, H, G, n - m, m, d, seed=23, dtype=torch.bfloat16, device=dev)
+    q, k, v = q.view(Lyr, B, H, m, d), k.view(Lyr, B, G, n, d), v.view(Lyr, B, G, n, d)
+    LB = 128 * G
+    ref = PL.compress_model(q, k, v, LB, reserve=3)
+    out = PL.compress_model(q, k, v, LB, reserve=3)
+    for t in (out.k, out.v):
+        t.zero_()
+    for t in (out.seg_start, out.seqlens, out.seg_cap, out.budgets):
+        t.fill_(-7)
+    vv = v.cpu().pin_memory() if host_v else v
+    comp, gst = torch.cuda.current_stream(), torch.cuda.Stream(device=dev)
+    nch, lc = 4, Lyr // 4
+    wsb = ops.compress_workspace_bytes(q[:lc].reshape(lc * B, H, m, d), k[:lc].reshape(lc * B, G, n, d))
+    wss = [torch.zeros(wsb, dtype=torch.uint8, device=dev) for _ in range(2)]
+    done = [torch.cuda.Event(), torch.cuda.Event()]
+    for c in range(nch):
+        if c >= 2:
+            comp.wait_event(done[c & 1])
+        sl = slice(c * lc, (c + 1) * lc)
+        PL.compress_model(q[sl], k[sl], vv[sl], LB, reserve=3, out=out, first_layer=c * lc, ws=wss[c & 1],
+                          gather_stream=gst)
+        done[c & 1].record(gst)
+    comp.wait_stream(gst)
+    for name in ("seg_start", "seqlens", "seg_cap", "budgets"):
+        assert torch.equal(getattr(out, name), getattr(ref, name)), name
+    st, ln = ref.seg_start.cpu().numpy(), ref.seqlens.cpu().numpy()
+    rows = torch.as_tensor(np.concatenate([np.arange(a, a + b) for a, b in zip(st, ln)]), device=dev)
+    assert torch.equal(out.k[rows].view(torch.int16), ref.k[rows].view(torch.int16))
+    assert torch.equal(out.v[rows].view(torch.int16), ref.v[rows].view(torch.int16))
+    for w in wss:
+        ops.workspace_status(w)
+    with pytest.raises(L.InvalidArgument):
+        ops.compress(q[0], k[0], v[0], LB, gather_stream=gst, check=True)
