@@ -81,6 +81,31 @@ def main():
     out["compress_ms_per_layer"] = t / P
     out["compress_gbs"] = bytes_c / (t * 1e-3) / 1e9
     out["compress_frac"] = out["compress_gbs"] / peak
+    # the same compress as 4 calls of P/4 layers (a prefill compressed as its layers arrive),
+    # with and without each chunk's gather forked onto a second stream (adakv_compress_split)
+    if P % 4 == 0 and not args.generic:
+        nch, lc = 4, P // 4
+        gst = torch.cuda.Stream()
+        wss = [torch.zeros(A.ops.compress_workspace_bytes(q[:lc], k[:lc]), dtype=torch.uint8, device=dev)
+               for _ in range(2)]
+        evs = [torch.cuda.Event(), torch.cuda.Event()]
+
+        def chunked(split):
+            cur = torch.cuda.current_stream()
+            if split:
+                gst.wait_stream(cur)
+            for c in range(nch):
+                if split and c >= 2:
+                    cur.wait_event(evs[c & 1])
+                sl = slice(c * lc, (c + 1) * lc)
+                A.compress(q[sl], k[sl], v[sl], LB, reserve=8, out=cache, ws=wss[c & 1], first_problem=c * lc,
+                           gather_stream=gst if split else None)
+                if split:
+                    evs[c & 1].record(gst)
+            if split:
+                cur.wait_stream(gst)
+        out["compress_4chunks_ms_per_layer"] = graph_time(lambda: chunked(False)) / P
+        out["compress_4chunks_split_gather_ms_per_layer"] = graph_time(lambda: chunked(True)) / P
     # select alone (scores already computed) -- via segmented_select on fp32 scores
     sc = gs.reshape(P, G * n_o)
     import numpy as np
