@@ -258,13 +258,15 @@ int main() {
     long long* d; cudaMalloc(&d, 64 * 64 * sizeof(long long));
     const int nslots = 3, nblk = 64;
     for (int mode : {0, 7, 8}) {
-        for (int W : {1, 2, 4, 8, 16}) {
-            const size_t smem = size_t(W) * nslots * 2 * kBoxBytes + 1024;
+        for (int W : {1, 2, 4, 8, 12, 16}) {
+            const int ns = W <= 8 ? nslots : (W <= 12 ? 2 : 1);  // the rings within 227 KB
+            const size_t smem = size_t(W) * ns * 2 * kBoxBytes + 1024;
             auto kern = mode == 0 ? k<0> : mode == 7 ? k<7> : k<8>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (smem > 227 * 1024) continue;
-            kern<<<1, 32 * W, smem>>>(d, nblk, nslots, 0.127f);
-            kern<<<1, 32 * W, smem>>>(d, nblk, nslots, 0.127f);
+            kern<<<1, 32 * W, smem>>>(d, nblk, ns, 0.127f);
+            kern<<<1, 32 * W, smem>>>(d, nblk, ns, 0.127f);
+            if (cudaGetLastError() != cudaSuccess) { printf("W=%d launch failed\n", W); continue; }
             long long h[64]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
             long long mx = 0; for (int w = 0; w < W; ++w) mx = h[w] > mx ? h[w] : mx;
             printf("mode %d (%s) W=%2d: %6.1f cycles/block/warp  (smem %.0f B/clk)\n", mode, mode == 0 ? "full" : mode == 1 ? "S+LDS" : mode == 2 ? "LDS" : mode == 3 ? "S^T full" : mode == 7 ? "vote-max" : "pairs", W,
