@@ -557,19 +557,19 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant
     // per-(warp, head) scales are the same for every column, so each lane of a merging warp
     // computes one of them (lane = 4 w + head; W = 8 covers the warp) and the column loop
     // reads them back as broadcast float4s instead of recomputing 32 exponentials per thread.
-    static_assert(W == 8, "one scale per lane: 8 warps x 4 heads");
+    static_assert(W <= 8, "one scale per lane: up to 8 warps x 4 heads");
     {
         const int nq = (gs + 3) >> 2;
         for (int t = threadIdx.x; t < 128 * nq; t += 32 * W) {
             const int hq = t >> 7, c = t & 127;  // head quad is uniform over a warp
             const int fw = lane >> 2, fh = 4 * hq + (lane & 3);
-            const float mw = S.s_ml[fw][fh][0];
+            const float mw = fw < W ? S.s_ml[fw][fh][0] : -INFINITY;
             float M = mw;
             M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 4));
             M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 8));
             M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 16));
             const float f = mw == -INFINITY ? 0.f : ex2f(mw - M);
-            float lf = S.s_ml[fw][fh][1] * f;
+            float lf = fw < W ? S.s_ml[fw][fh][1] * f : 0.f;
             lf += __shfl_xor_sync(0xffffffffu, lf, 4);
             lf += __shfl_xor_sync(0xffffffffu, lf, 8);
             lf += __shfl_xor_sync(0xffffffffu, lf, 16);  // lanes 0..3: the head's scaled sum

@@ -3,6 +3,7 @@
 // swizzled K/V box; prints cycles per block for W = 1, 2, 4, 8.  Variants: full body,
 // S only (no softmax/PV), LDS only.
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_bf16.h>
 
@@ -18,7 +19,7 @@ __device__ __forceinline__ uint32_t box_off(int r, int c) { const int line = 2 *
 __device__ __forceinline__ int kperm(int n) { const int t = n >> 1, e = n & 1; return (e << 2) | (t ^ (e << 1)); }
 
 template <int MODE>
-__global__ void k(long long* out, int nblk, int nslots, float scale_log2) {
+__global__ void k(long long* out, int nblk, int nslots, float scale_log2, int reps) {
     extern __shared__ __align__(1024) uint8_t sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
     for (int i = threadIdx.x; i < (int)(blockDim.x / 32) * nslots * 2 * kBoxBytes / 4; i += blockDim.x)
@@ -34,7 +35,9 @@ __global__ void k(long long* out, int nblk, int nslots, float scale_log2) {
     float m_run = -INFINITY, l_run = 0.f, acc[8][4] = {};
     float sink = 0.f;
     __syncthreads();
-    const long long t0 = clock64();
+    long long t0 = clock64();
+    for (int rep = 0; rep < reps; ++rep) {
+    if (rep == reps - 1) t0 = clock64();
     if (MODE == 3 || MODE == 6) {
         // K as the A operand (rows = keys): lane reads row gid and gid+8, 4 chunks each
         uint32_t ka[2][4];
@@ -249,6 +252,7 @@ __global__ void k(long long* out, int nblk, int nslots, float scale_log2) {
         __syncwarp();
     }
     for (int i = 0; i < 8; ++i) sink += acc[i][0] + acc[i][3];
+    }  // reps
     const long long t1 = clock64();
     if (lane == 0) out[blockIdx.x * 64 + warp] = t1 - t0;
     if (sink == 1234.5f + l_run) out[0] = 0;
@@ -256,16 +260,18 @@ __global__ void k(long long* out, int nblk, int nslots, float scale_log2) {
 
 int main() {
     long long* d; cudaMalloc(&d, 64 * 64 * sizeof(long long));
-    const int nslots = 3, nblk = 64;
-    for (int mode : {0, 7, 8}) {
+    const int nslots = 3;
+    const int nblk = getenv("NBLK") ? atoi(getenv("NBLK")) : 64;
+    const int reps = getenv("REPS") ? atoi(getenv("REPS")) : 1;
+    for (int mode : {0, 1, 2, 7, 8}) {
         for (int W : {1, 2, 4, 8, 12, 16}) {
             const int ns = W <= 8 ? nslots : (W <= 12 ? 2 : 1);  // the rings within 227 KB
             const size_t smem = size_t(W) * ns * 2 * kBoxBytes + 1024;
-            auto kern = mode == 0 ? k<0> : mode == 7 ? k<7> : k<8>;
+            auto kern = mode == 0 ? k<0> : mode == 1 ? k<1> : mode == 2 ? k<2> : mode == 7 ? k<7> : k<8>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (smem > 227 * 1024) continue;
-            kern<<<1, 32 * W, smem>>>(d, nblk, ns, 0.127f);
-            kern<<<1, 32 * W, smem>>>(d, nblk, ns, 0.127f);
+            kern<<<1, 32 * W, smem>>>(d, nblk, ns, 0.127f, reps);
+            kern<<<1, 32 * W, smem>>>(d, nblk, ns, 0.127f, reps);
             if (cudaGetLastError() != cudaSuccess) { printf("W=%d launch failed\n", W); continue; }
             long long h[64]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
             long long mx = 0; for (int w = 0; w < W; ++w) mx = h[w] > mx ? h[w] : mx;
