@@ -34,6 +34,7 @@ namespace {
 
 constexpr int kSelThreads = 1024;
 constexpr int kWarps = kSelThreads / 32;
+constexpr int kEChunks = 8;  // phase E: 32-key chunks per warp with their loads in flight
 
 enum SegMode : int { MODE_NONE = 0, MODE_ALL = 1, MODE_THRESH = 2, MODE_STREAM = 3 };
 
@@ -210,6 +211,35 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         for (int64_t i = h0 + nv * V + tid; i < len; i += kSelThreads) kc[i] = KeyOf<F>::get(src[i]);
     }
     auto key_at = [&](int64_t e) -> KT { return cached ? kc[e - lo] : KeyOf<F>::get(sc[e]); };
+    // Uncached slices (too large for shared memory): every key of [a, b) from global memory
+    // (L2) through fn(e, key), 16-byte loads with four per thread in flight; the unaligned
+    // head and tail elements are read singly so no load leaves [a, b).
+    auto scan_global = [&](int64_t a, int64_t b, auto&& fn) {
+        constexpr int V = 16 / int(sizeof(F));
+        const int64_t mis = int64_t(reinterpret_cast<uintptr_t>(sc + a) / sizeof(F)) % V;
+        const int64_t va = min(b, a + (V - mis) % V);  // first vector-aligned element
+        const int64_t nv = (b - va) / V;
+        const int64_t vb = va + nv * V;
+        for (int64_t e = a + tid; e < va; e += kSelThreads) fn(e, KeyOf<F>::get(sc[e]));
+        for (int64_t e = vb + tid; e < b; e += kSelThreads) fn(e, KeyOf<F>::get(sc[e]));
+        const uint4* vs = reinterpret_cast<const uint4*>(sc + va);
+        for (int64_t t0 = tid; t0 < nv; t0 += 4 * kSelThreads) {
+            uint4 r[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t t = t0 + int64_t(u) * kSelThreads;
+                r[u] = t < nv ? __ldcg(vs + t) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t t = t0 + int64_t(u) * kSelThreads;
+                if (t >= nv) break;
+                const F* f = reinterpret_cast<const F*>(&r[u]);
+#pragma unroll
+                for (int c = 0; c < V; ++c) fn(va + t * V + c, KeyOf<F>::get(f[c]));
+            }
+        }
+    };
     __syncthreads();
     stamp();
     if (tid == 0) {
@@ -235,11 +265,14 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     __shared__ int s_top;
     {
         KT mn = ~KT(0), mx = KT(0);
-        for (int64_t e = lo + tid; e < hi; e += kSelThreads) {
-            const KT u = key_at(e);
+        auto fold = [&](int64_t, KT u) {
             mn = u < mn ? u : mn;
             mx = u > mx ? u : mx;
-        }
+        };
+        if (cached)
+            for (int64_t e = lo + tid; e < hi; e += kSelThreads) fold(e, kc[e - lo]);
+        else
+            scan_global(lo, hi, fold);
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
             const KT a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
@@ -330,15 +363,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                     }
                 }
             } else {
-                for (int64_t base = a; base < b; base += kSelThreads) {
-                    const int64_t e = base + tid;
-                    int key = -1;
-                    if (e < b) {
-                        const KT u = key_at(e);
-                        if ((u & mask) == pre) key = int((u >> shift) & 0xFF);
-                    }
-                    if (key >= 0) atomicAdd(&my[key], 1u);  // warp-private: only intra-warp collisions
-                }
+                scan_global(a, b, [&](int64_t, KT u) {
+                    if ((u & mask) == pre) atomicAdd(&my[int((u >> shift) & 0xFF)], 1u);  // warp-private histogram
+                });
             }
             fstamp(1);
             __syncthreads();
@@ -569,21 +596,23 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         uint32_t gt = 0, eq = 0;
         if (mode == MODE_THRESH) {
             const KT T = seg_T[s];
-            // four chunks' loads in flight before any compare
-            for (int64_t base = a; base < b; base += 128) {
-                KT u[4];
+            // kEChunks chunks' loads in flight before any compare; per-lane counts, one warp sum
+            for (int64_t base = a; base < b; base += 32 * kEChunks) {
+                KT u[kEChunks];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
+                for (int c = 0; c < kEChunks; ++c) {
                     const int64_t e = base + c * 32 + lane;
                     u[c] = e < b ? key_at(e) : KT(0);
                 }
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
+                for (int c = 0; c < kEChunks; ++c) {
                     const bool ok = base + c * 32 + lane < b;
-                    gt += __popc(__ballot_sync(0xffffffffu, ok && u[c] > T));
-                    eq += __popc(__ballot_sync(0xffffffffu, ok && u[c] == T));
+                    gt += (ok && u[c] > T) ? 1u : 0u;
+                    eq += (ok && u[c] == T) ? 1u : 0u;
                 }
             }
+            gt = __reduce_add_sync(0xffffffffu, gt);
+            eq = __reduce_add_sync(0xffffffffu, eq);
         } else if (mode == MODE_ALL) {
             gt = uint32_t(b - a);
         } else if (mode == MODE_STREAM) {
@@ -702,16 +731,16 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                 run_kept += __popc(bk);
             };
             if (mode == MODE_THRESH) {
-                // four chunks' key loads issued ahead of the stores (which may alias them)
-                for (int o = 0; o < len; o += 128) {
-                    KT u[4];
+                // kEChunks chunks' key loads issued ahead of the stores (which may alias them)
+                for (int o = 0; o < len; o += 32 * kEChunks) {
+                    KT u[kEChunks];
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
+                    for (int c = 0; c < kEChunks; ++c) {
                         const int j = o + c * 32 + lane;
                         u[c] = j < len ? key_at(a + j) : KT(0);
                     }
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
+                    for (int c = 0; c < kEChunks; ++c) {
                         if (o + c * 32 >= len) break;  // warp-uniform
                         const int j = o + c * 32 + lane;
                         const bool valid = j < len;

@@ -13,7 +13,7 @@ from paper_2407_11550_b200.synthetic import planted_layer  # noqa: E402
 L = A.lib()
 dev = torch.device("cuda:0")
 P = int(os.environ.get("P", "1"))
-H, G, m, d, n = 32, 8, 32, 128, 32768
+H, G, m, d, n = 32, 8, 32, 128, int(os.environ.get("PROMPT", "32768"))
 q, k, v = planted_layer(P, H, G, n - m, m, d, seed=3, dtype=torch.bfloat16, device=dev)
 A.compress(q, k, v, 16384, reserve=64)
 torch.cuda.synchronize()
