@@ -19,6 +19,10 @@
 // masks and kept positions are bit-identical to the reference on identical scores.
 #include <cooperative_groups.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "select.cuh"
 
 namespace cg = cooperative_groups;
@@ -35,6 +39,7 @@ namespace {
 constexpr int kSelThreads = 1024;
 constexpr int kWarps = kSelThreads / 32;
 constexpr int kEChunks = 8;  // phase E: 32-key chunks per warp with their loads in flight
+constexpr int kMaxSelCS = 16;  // CTAs per cluster (16 needs the non-portable cluster size)
 
 enum SegMode : int { MODE_NONE = 0, MODE_ALL = 1, MODE_THRESH = 2, MODE_STREAM = 3 };
 
@@ -295,17 +300,19 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         }
         cluster.sync();
         if (tid == 0) {
-            KT v[2][8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                v[0][r] = unsigned(r) < CS ? cluster.map_shared_rank(cta_mm, r)[0] : ~KT(0);
-                v[1][r] = unsigned(r) < CS ? cluster.map_shared_rank(cta_mm, r)[1] : KT(0);
-            }
             KT a = ~KT(0), b = KT(0);
+            for (int rb = 0; rb < int(CS); rb += 8) {
+                KT v[2][8];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                a = v[0][r] < a ? v[0][r] : a;
-                b = v[1][r] > b ? v[1][r] : b;
+                for (int r = 0; r < 8; ++r) {
+                    v[0][r] = unsigned(rb + r) < CS ? cluster.map_shared_rank(cta_mm, rb + r)[0] : ~KT(0);
+                    v[1][r] = unsigned(rb + r) < CS ? cluster.map_shared_rank(cta_mm, rb + r)[1] : KT(0);
+                }
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    a = v[0][r] < a ? v[0][r] : a;
+                    b = v[1][r] > b ? v[1][r] : b;
+                }
             }
             // empty problem slices leave a > b; any top works then
             const KT x = a <= b ? (a ^ b) : KT(0);
@@ -384,22 +391,34 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         // sum the CS histograms through DSMEM: all remote loads issued before any is used
         // (segment s has elements only in ranks [r0, r1]: the others' histograms are zero)
         for (int i0 = tid; i0 < S * 256; i0 += 2 * kSelThreads) {
-            uint32_t v[2][8];
+            uint32_t t[2] = {0u, 0u};
+            unsigned r0[2], r1[2];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const int i = i0 + u * kSelThreads;
-                const int sg = i >> 8;
                 const bool in = i < S * 256;
-                const unsigned r0 = in ? seg_r0[sg] : 1u, r1 = in ? seg_r1[sg] : 0u;
+                r0[u] = in ? seg_r0[i >> 8] : 1u;
+                r1[u] = in ? seg_r1[i >> 8] : 0u;
+            }
+            // eight ranks per round (a segment spans more only in clusters of more than 8)
+            for (unsigned rb = 0; rb < CS; rb += 8) {
+                if (r0[0] + rb > r1[0] && r0[1] + rb > r1[1]) break;
+                uint32_t v[2][8];
 #pragma unroll
-                for (int r = 0; r < 8; ++r)
-                    v[u][r] = (unsigned(r) + r0 <= r1) ? cluster.map_shared_rank(hb, r0 + r)[i] : 0u;
+                for (int u = 0; u < 2; ++u) {
+                    const int i = i0 + u * kSelThreads;
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+                        v[u][r] = (r0[u] + rb + unsigned(r) <= r1[u]) ? cluster.map_shared_rank(hb, r0[u] + rb + r)[i] : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+                    t[u] += ((v[u][0] + v[u][1]) + (v[u][2] + v[u][3])) + ((v[u][4] + v[u][5]) + (v[u][6] + v[u][7]));
             }
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const int i = i0 + u * kSelThreads;
-                if (i < S * 256)
-                    agg[i] = ((v[u][0] + v[u][1]) + (v[u][2] + v[u][3])) + ((v[u][4] + v[u][5]) + (v[u][6] + v[u][7]));
+                if (i < S * 256) agg[i] = t[u];
             }
         }
         fstamp(5);
@@ -647,22 +666,24 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     for (int s = tid; s < S; s += kSelThreads) {
         int64_t eqb = 0, kept = 0;
         const int64_t need = seg_mode[s] == MODE_THRESH ? seg_need[s] : 0;
-        uint32_t rg[8], rq[8];  // every lower rank's counts, all remote loads in flight at once
+        for (unsigned rb = 0; rb < rank; rb += 8) {
+            uint32_t rg[8], rq[8];  // eight lower ranks' counts per round, their remote loads in flight at once
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            rg[r] = rq[r] = 0u;
-            if (unsigned(r) < rank) {
-                const uint32_t* rc = cluster.map_shared_rank(&ccnt[0][0], r);
-                rg[r] = rc[s * 2 + 0];
-                rq[r] = rc[s * 2 + 1];
+            for (int r = 0; r < 8; ++r) {
+                rg[r] = rq[r] = 0u;
+                if (rb + unsigned(r) < rank) {
+                    const uint32_t* rc = cluster.map_shared_rank(&ccnt[0][0], rb + r);
+                    rg[r] = rc[s * 2 + 0];
+                    rq[r] = rc[s * 2 + 1];
+                }
             }
-        }
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int64_t g = rg[r], q = rq[r];
-            const int64_t t = need - eqb;
-            kept += g + (t <= 0 ? 0 : (t < q ? t : q));
-            eqb += q;
+            for (int r = 0; r < 8; ++r) {
+                const int64_t g = rg[r], q = rq[r];
+                const int64_t t = need - eqb;
+                kept += g + (t <= 0 ? 0 : (t < q ? t : q));
+                eqb += q;
+            }
         }
         seg_eqb[s] = eqb;
         seg_kept_before[s] = kept;
@@ -777,17 +798,71 @@ size_t select_smem_bytes(int S) {
 }
 constexpr size_t kSelSmemCap = 220 * 1024;  // dynamic shared memory budget per CTA
 
-adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStream_t stream) {
-    if (P == 0) return ADAKV_OK;
-    const int64_t per_cta = 16384;
-    int CS = int(ceil_div(prm.N, per_cta));
-    CS = CS < 1 ? 1 : (CS > 8 ? 8 : CS);
-    if (const char* e = std::getenv("ADAKV_SELECT_CS")) CS = std::max(1, std::min(8, std::atoi(e)));
+// dynamic shared memory of a select launch with CS CTAs per cluster; sets cache_keys
+static size_t select_launch_smem(bool key64, const SelParams& prm, int CS, int* cache_keys) {
     size_t smem = select_smem_bytes(prm.S);
     const size_t key_bytes = size_t(ceil_div(prm.N, CS)) * (key64 ? 8 : 4) + 16;  // + vector-read slack
+    *cache_keys = smem + key_bytes <= kSelSmemCap;
+    return *cache_keys ? smem + key_bytes : smem;
+}
+
+template <class F>
+static cudaError_t select_prepare(size_t smem) {
+    cudaError_t e = cudaFuncSetAttribute(select_kernel<F>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(select_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    return e;
+}
+
+// clusters of CS CTAs (smem bytes each) the device holds at once
+static int select_fit(bool key64, int CS, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, bool, int, size_t>, int> memo;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(dev, key64, CS, smem);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+    int n = 0;
+    if ((key64 ? select_prepare<double>(smem) : select_prepare<float>(smem)) == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(CS));
+        cfg.blockDim = dim3(kSelThreads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = unsigned(CS);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (key64 ? cudaOccupancyMaxActiveClusters(&n, select_kernel<double>, &cfg) != cudaSuccess
+                  : cudaOccupancyMaxActiveClusters(&n, select_kernel<float>, &cfg) != cudaSuccess)
+            n = 0;
+    }
+    cudaGetLastError();
+    memo[key] = n;
+    return n;
+}
+
+adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStream_t stream) {
+    if (P == 0) return ADAKV_OK;
+    // ~16K keys per CTA (cached in shared memory up to ~50K), at most 8 CTAs per cluster; a
+    // problem too large for that takes up to 16 when the whole call still fits in one wave
+    const int64_t per_cta = 16384;
+    const int64_t want = ceil_div(prm.N, per_cta);
+    int CS = int(want < 1 ? 1 : (want > 8 ? 8 : want));
+    int cache_keys = 0;
+    for (int c = int(want < kMaxSelCS ? want : kMaxSelCS); c > 8; --c) {
+        if (select_fit(key64, c, select_launch_smem(key64, prm, c, &cache_keys)) >= P) {
+            CS = c;
+            break;
+        }
+    }
+    if (const char* e = std::getenv("ADAKV_SELECT_CS")) CS = std::max(1, std::min(kMaxSelCS, std::atoi(e)));
+    const size_t smem = select_launch_smem(key64, prm, CS, &cache_keys);
     SelParams lp = prm;
-    lp.cache_keys = smem + key_bytes <= kSelSmemCap;
-    if (lp.cache_keys) smem += key_bytes;
+    lp.cache_keys = cache_keys;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(P * CS));
     cfg.blockDim = dim3(kSelThreads);
@@ -801,10 +876,10 @@ adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStre
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (key64) {
-        ADAKV_CUDA_TRY(cudaFuncSetAttribute(select_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        ADAKV_CUDA_TRY(select_prepare<double>(smem));
         ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel<double>, lp, g_sel_dbg));
     } else {
-        ADAKV_CUDA_TRY(cudaFuncSetAttribute(select_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        ADAKV_CUDA_TRY(select_prepare<float>(smem));
         ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel<float>, lp, g_sel_dbg));
     }
     return ADAKV_OK;

@@ -210,3 +210,30 @@ def test_compress_split_gather_chunks_match_one_call(dev, host_v):
         ops.workspace_status(w)
     with pytest.raises(L.InvalidArgument):
         ops.compress(q[0], k[0], v[0], LB, gather_stream=gst, check=True)
+
+
+@pytest.mark.parametrize("cs", [None, "4"])
+@pytest.mark.parametrize("seg", [[0, 300000], list(np.linspace(0, 300000, 9).astype(int)),
+                                 [0, 7, 140001, 140002, 299990, 300000]])
+def test_select_sixteen_cta_cluster_matches_oracle(dev, oracle_mod, seg, cs, monkeypatch):
+    """A problem of 300K keys (one problem per call) takes a 16-CTA cluster (keys cached in
+    shared memory): DSMEM histogram sums over more than eight ranks, ragged segments across rank
+    boundaries.  Forced to 4 CTAs (ADAKV_SELECT_CS) the 75K-key slices are read from global
+    memory instead.  Blended adaptive budgets and keep masks bit-exact to evict_rows."""
+    if cs is not None:
+        monkeypatch.setenv("ADAKV_SELECT_CS", cs)
+    O = oracle_mod
+    rng = np.random.default_rng(len(seg))
+    off = np.asarray(seg, np.int64)
+    S = off.size - 1
+    x = np.round(rng.exponential(size=(1, 300000)) * 64) / 64  # heavy ties
+    s = torch.as_tensor(x, dtype=torch.float32, device=dev)
+    rows = [x[0, off[i]:off[i + 1]] for i in range(S)]
+    for total in (S + 5, 20000, 150001):
+        r = A.segmented_select(s, off, total, "adaptive", blend=True, alpha=0.2, repair=True)
+        alloc, keep = O.evict_rows(rows, total, True, 0.2)
+        assert r["budgets"][0].cpu().tolist() == alloc.tolist(), total
+        assert np.array_equal(r["keep"][0].cpu().numpy(), np.concatenate(keep)), total
+        kp = np.concatenate([np.nonzero(k)[0] for k in keep])
+        assert np.array_equal(r["kept_pos"][0, :total].cpu().numpy(), kp), total
+        A.workspace_status(r["ws"])
