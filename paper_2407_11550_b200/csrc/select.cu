@@ -847,13 +847,16 @@ static int select_fit(bool key64, int CS, size_t smem) {
 
 adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStream_t stream) {
     if (P == 0) return ADAKV_OK;
-    // ~16K keys per CTA (cached in shared memory up to ~50K), at most 8 CTAs per cluster; a
-    // problem too large for that takes up to 16 when the whole call still fits in one wave
+    // Cluster size: the largest (<= 16, and no more than ~16K keys per CTA) for which every
+    // problem of the call is resident at once -- one wave; a problem's latency is mostly its
+    // per-pass barriers, so one wave of smaller clusters beats two of larger ones (config 2,
+    // 32 problems of 262K keys: 4 CTAs streaming their slices from L2, 124 us, against 8 CTAs
+    // with the keys in shared memory in two waves, 207 us).  No size fits one wave: up to 8.
     const int64_t per_cta = 16384;
     const int64_t want = ceil_div(prm.N, per_cta);
     int CS = int(want < 1 ? 1 : (want > 8 ? 8 : want));
     int cache_keys = 0;
-    for (int c = int(want < kMaxSelCS ? want : kMaxSelCS); c > 8; --c) {
+    for (int c = int(want < 1 ? 1 : (want < kMaxSelCS ? want : kMaxSelCS)); c >= 1; --c) {
         if (select_fit(key64, c, select_launch_smem(key64, prm, c, &cache_keys)) >= P) {
             CS = c;
             break;
