@@ -82,7 +82,7 @@ def test_config3_every_request_scores(dev):
         assert e <= 1e-4, (p, e)
 
 
-@pytest.mark.parametrize("H,G", [(8, 8), (16, 8), (24, 8), (32, 8), (64, 8)])
+@pytest.mark.parametrize("H,G", [(8, 8), (16, 8), (24, 8), (32, 8), (48, 8), (64, 8)])
 def test_tc_scoring_group_sizes(dev, H, G):
     """The tcgen05 scoring kernel at g = H/G = 1, 2, 3, 4 (g*m = 32..128 window rows per
     UMMA tile; rows past g*m are idle lanes) and g = 8 (Llama-70B: 256 window rows, scored as
