@@ -644,7 +644,7 @@ adakv_status make_cache_map(CUtensorMap* m, const void* plane, int64_t rows) {
 
 }  // namespace
 
-// debug: per-CTA phase timestamps (ADAKV_DECODE_DEBUG=1), exported for scripts/dec_ts.py
+// debug: per-CTA phase timestamps, 64 slots per CTA (scripts/dec_ts4.py sets the buffer)
 static unsigned long long* g_dbg = nullptr;
 unsigned long long* dbg_buf() { return g_dbg; }
 extern "C" void adakv_debug_set_decode_timestamps(void* buf) { g_dbg = static_cast<unsigned long long*>(buf); }
