@@ -396,10 +396,10 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             const int o = q * 32 + lane;
             const int key = rt * prm.step + o;
             if (o < prm.step && key < prm.n_o) {
-                const int gpg = prm.pg_base + rpg;           // virtual group
-                const int gvirt = prm.G * prm.vsplit;
-                const int p = gpg / gvirt, gv = gpg % gvirt;
-                const int g = gv / prm.vsplit, h0 = (gv % prm.vsplit) * prm.gs;  // first head of the tile
+                // virtual group gpg = (p G + g) vsplit + half holds heads [gpg gs, gpg gs + gs) of
+                // all H = G gs vsplit, and group row p G + g = gpg / vsplit (vsplit = 1, 2, 4): no
+                // division by G per readout
+                const int gpg = prm.pg_base + rpg;
                 constexpr float inv_scale = 1.f / 65536.f;
                 float gsum = 0.f;
 #pragma unroll
@@ -407,10 +407,9 @@ score_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                     if (h >= prm.gs) break;
                     const float sh = hv[h] * inv_scale;
                     gsum += sh;
-                    if (prm.head_scores)
-                        prm.head_scores[(size_t(p) * prm.H + g * prm.gs * prm.vsplit + h0 + h) * prm.n_o + key] = sh;
+                    if (prm.head_scores) prm.head_scores[(size_t(gpg) * prm.gs + h) * prm.n_o + key] = sh;
                 }
-                float* gdst = prm.group_scores + (size_t(p) * prm.G + g) * prm.n_o + key;
+                float* gdst = prm.group_scores + size_t(gpg >> (prm.vsplit >> 1)) * prm.n_o + key;
                 if (prm.vsplit == 1) *gdst = gsum * prm.inv_g;
                 else atomicAdd(gdst, gsum * prm.inv_g);
             }
