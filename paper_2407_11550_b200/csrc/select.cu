@@ -798,19 +798,42 @@ size_t select_smem_bytes(int S) {
 }
 constexpr size_t kSelSmemCap = 220 * 1024;  // dynamic shared memory budget per CTA
 
-// dynamic shared memory of a select launch with CS CTAs per cluster; sets cache_keys
-static size_t select_launch_smem(bool key64, const SelParams& prm, int CS, int* cache_keys) {
-    size_t smem = select_smem_bytes(prm.S);
-    const size_t key_bytes = size_t(ceil_div(prm.N, CS)) * (key64 ? 8 : 4) + 16;  // + vector-read slack
-    *cache_keys = smem + key_bytes <= kSelSmemCap;
-    return *cache_keys ? smem + key_bytes : smem;
+// The kernels' attributes are set once per device, to the most dynamic shared memory the
+// device allows beside their static shared memory (and non-portable cluster sizes), so no
+// launch ever changes them (concurrent launches of different sizes cannot race).
+template <class F>
+static cudaError_t select_prepare(size_t* max_dyn) {
+    static std::mutex mu;
+    static size_t cap[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < 64 && cap[dev]) {
+        *max_dyn = cap[dev];
+        return cudaSuccess;
+    }
+    cudaFuncAttributes fa{};
+    int optin = 0;
+    e = cudaFuncGetAttributes(&fa, select_kernel<F>);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const size_t c = std::min(kSelSmemCap, size_t(optin) - fa.sharedSizeBytes);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(select_kernel<F>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(select_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(c));
+    if (e == cudaSuccess && dev < 64) cap[dev] = c;
+    *max_dyn = c;
+    return e;
+}
+static cudaError_t select_prepare(bool key64, size_t* max_dyn) {
+    return key64 ? select_prepare<double>(max_dyn) : select_prepare<float>(max_dyn);
 }
 
-template <class F>
-static cudaError_t select_prepare(size_t smem) {
-    cudaError_t e = cudaFuncSetAttribute(select_kernel<F>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(select_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    return e;
+// dynamic shared memory of a select launch with CS CTAs per cluster; sets cache_keys
+static size_t select_launch_smem(bool key64, const SelParams& prm, int CS, size_t max_dyn, int* cache_keys) {
+    size_t smem = select_smem_bytes(prm.S);
+    const size_t key_bytes = size_t(ceil_div(prm.N, CS)) * (key64 ? 8 : 4) + 16;  // + vector-read slack
+    *cache_keys = smem + key_bytes <= max_dyn;
+    return *cache_keys ? smem + key_bytes : smem;
 }
 
 // clusters of CS CTAs (smem bytes each) the device holds at once
@@ -824,7 +847,8 @@ static int select_fit(bool key64, int CS, size_t smem) {
     auto it = memo.find(key);
     if (it != memo.end()) return it->second;
     int n = 0;
-    if ((key64 ? select_prepare<double>(smem) : select_prepare<float>(smem)) == cudaSuccess) {
+    size_t max_dyn = 0;
+    if (select_prepare(key64, &max_dyn) == cudaSuccess) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(unsigned(CS));
         cfg.blockDim = dim3(kSelThreads);
@@ -855,15 +879,21 @@ adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStre
     const int64_t per_cta = 16384;
     const int64_t want = ceil_div(prm.N, per_cta);
     int CS = int(want < 1 ? 1 : (want > 8 ? 8 : want));
+    size_t max_dyn = 0;
+    ADAKV_CUDA_TRY(select_prepare(key64, &max_dyn));
+    // per-segment histograms (~4.75 KB per segment) beside the per-warp ones: on B200 at most 39
+    // segments (KV groups) per problem fit one CTA's shared memory
+    if (select_smem_bytes(prm.S) > max_dyn)
+        return fail(ADAKV_UNSUPPORTED, "selection: too many segments (KV groups) per problem for shared memory");
     int cache_keys = 0;
     for (int c = int(want < 1 ? 1 : (want < kMaxSelCS ? want : kMaxSelCS)); c >= 1; --c) {
-        if (select_fit(key64, c, select_launch_smem(key64, prm, c, &cache_keys)) >= P) {
+        if (select_fit(key64, c, select_launch_smem(key64, prm, c, max_dyn, &cache_keys)) >= P) {
             CS = c;
             break;
         }
     }
     if (const char* e = std::getenv("ADAKV_SELECT_CS")) CS = std::max(1, std::min(kMaxSelCS, std::atoi(e)));
-    const size_t smem = select_launch_smem(key64, prm, CS, &cache_keys);
+    const size_t smem = select_launch_smem(key64, prm, CS, max_dyn, &cache_keys);
     SelParams lp = prm;
     lp.cache_keys = cache_keys;
     cudaLaunchConfig_t cfg = {};
@@ -878,13 +908,8 @@ adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStre
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (key64) {
-        ADAKV_CUDA_TRY(select_prepare<double>(smem));
-        ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel<double>, lp, g_sel_dbg));
-    } else {
-        ADAKV_CUDA_TRY(select_prepare<float>(smem));
-        ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel<float>, lp, g_sel_dbg));
-    }
+    if (key64) ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel<double>, lp, g_sel_dbg));
+    else ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel<float>, lp, g_sel_dbg));
     return ADAKV_OK;
 }
 

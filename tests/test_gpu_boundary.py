@@ -237,3 +237,13 @@ def test_select_sixteen_cta_cluster_matches_oracle(dev, oracle_mod, seg, cs, mon
         kp = np.concatenate([np.nonzero(k)[0] for k in keep])
         assert np.array_equal(r["kept_pos"][0, :total].cpu().numpy(), kp), total
         A.workspace_status(r["ws"])
+
+
+def test_select_segment_limit_is_reported(dev):
+    """More segments per problem than one CTA's shared memory holds (39 on B200) is a clean
+    ADAKV_UNSUPPORTED, not a launch failure; 39 work."""
+    s = torch.rand((1, 64 * 100), device=dev)
+    with pytest.raises(L.AdaKVError, match="too many segments"):
+        A.segmented_select(s, np.arange(65) * 100, 640, "adaptive")
+    r = A.segmented_select(s[:, :3900], np.arange(40) * 100, 640, "adaptive")
+    assert int(r["budgets"].sum()) == 640
