@@ -204,9 +204,9 @@ adakv_status adakv_window_scores_workspace(adakv_dtype dtype, const adakv_layer_
  * per-segment select).  S segments per problem, ragged: segment s is
  * scores[p*off[S] + off[s] .. + off[s+1]).  Keys are f32 or f64 (exact order,
  * -0 == +0; NaN not allowed).  Order (score desc, segment asc, position asc).
- * S is limited by one CTA's shared memory (per-segment histograms, ~4.75 KB per
- * segment): on B200 at most 39 segments -- KV groups, for adakv_compress -- per
- * problem; more return ADAKV_UNSUPPORTED.
+ * S (<= 64: KV groups, for adakv_compress) is held in one CTA's shared memory as
+ * per-segment histograms; beyond ~39 segments on B200 a leaner layout with one
+ * more cluster barrier per radix pass is used.
  * ------------------------------------------------------------------------- */
 typedef enum adakv_alloc_mode {
     ADAKV_ALLOC_ADAPTIVE = 0, /* adaptive_allocation (budget.hpp:118-140) [+ safeguard_blend] */

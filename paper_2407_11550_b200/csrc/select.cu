@@ -118,10 +118,11 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     const int64_t lo = N * rank / CS, hi = N * (rank + 1) / CS;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);     // [2][S][256]
-    uint32_t* agg = hist + 2 * S * 256;                          // [S][256]
-    uint32_t* hist0 = agg + S * 256;                             // [S][256]
-    uint32_t* wcnt = hist0 + S * 256;                            // [kWarps][S][2]
+    const bool lean = prm.lean != 0;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);     // [2][S][256] ([1] when lean)
+    uint32_t* agg = hist + (lean ? 1 : 2) * S * 256;             // [S][256]
+    uint32_t* hist0 = agg + S * 256;                             // [S][256] (none when lean)
+    uint32_t* wcnt = hist0 + (lean ? 0 : S * 256);               // [kWarps][S][2]
     int64_t* wkept = reinterpret_cast<int64_t*>(wcnt + kWarps * S * 2);  // [kWarps][S]
     int64_t* weqb = wkept + kWarps * S;                                  // [kWarps][S]
     uint32_t* wh = reinterpret_cast<uint32_t*>(weqb + kWarps * S);       // [kWarps][256] per-warp histograms
@@ -333,8 +334,13 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
     // One radix digit over all segments with seg_active[s] set: per-segment
     // histograms of elements matching that segment's prefix, cluster-summed into agg.
     int buf = 0;  // histogram double buffer; toggled only by a pass that used it
+    bool hist_used = false;
     auto radix_pass = [&](int pass) {
         fine_pass = pass;
+        // one buffer: every rank has finished reading this CTA's previous histograms
+        if (lean && hist_used) cluster.sync();
+        hist_used = true;
+        if (lean) buf = 0;
         fstamp(0);
         const int shift = lo_bit(pass);
         const KT mask = hi_mask(pass);
@@ -444,8 +450,10 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
             __syncthreads();
             radix_pass(pass);
             if (pass == 0) {
-                for (int i = tid; i < S * 256; i += kSelThreads) hist0[i] = agg[i];
-                if (tid == 0) have_hist0 = 1;
+                if (!lean) {
+                    for (int i = tid; i < S * 256; i += kSelThreads) hist0[i] = agg[i];
+                    if (tid == 0) have_hist0 = 1;
+                }
             }
             __shared__ int g_bin;
             __shared__ uint32_t gsum[256];
@@ -796,6 +804,10 @@ size_t select_smem_bytes(int S) {
     return size_t(4) * (2 * S * 256 + S * 256 + S * 256 + kWarps * S * 2) + size_t(8) * 2 * kWarps * S +
            size_t(4) * kWarps * 256;
 }
+// the same without the second histogram buffer and the kept first-digit histograms (lean)
+size_t select_smem_bytes_lean(int S) {
+    return select_smem_bytes(S) - size_t(4) * 2 * S * 256;
+}
 constexpr size_t kSelSmemCap = 220 * 1024;  // dynamic shared memory budget per CTA
 
 // The kernels' attributes are set once per device, to the most dynamic shared memory the
@@ -830,7 +842,7 @@ static cudaError_t select_prepare(bool key64, size_t* max_dyn) {
 
 // dynamic shared memory of a select launch with CS CTAs per cluster; sets cache_keys
 static size_t select_launch_smem(bool key64, const SelParams& prm, int CS, size_t max_dyn, int* cache_keys) {
-    size_t smem = select_smem_bytes(prm.S);
+    size_t smem = prm.lean ? select_smem_bytes_lean(prm.S) : select_smem_bytes(prm.S);
     const size_t key_bytes = size_t(ceil_div(prm.N, CS)) * (key64 ? 8 : 4) + 16;  // + vector-read slack
     *cache_keys = smem + key_bytes <= max_dyn;
     return *cache_keys ? smem + key_bytes : smem;
@@ -881,20 +893,22 @@ adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStre
     int CS = int(want < 1 ? 1 : (want > 8 ? 8 : want));
     size_t max_dyn = 0;
     ADAKV_CUDA_TRY(select_prepare(key64, &max_dyn));
-    // per-segment histograms (~4.75 KB per segment) beside the per-warp ones: on B200 at most 39
-    // segments (KV groups) per problem fit one CTA's shared memory
-    if (select_smem_bytes(prm.S) > max_dyn)
+    // per-segment histograms (~4.75 KB per segment) beside the per-warp ones fit up to 39
+    // segments (KV groups) per problem on B200; more take the lean layout (~2.75 KB per
+    // segment, up to 68: one histogram buffer and an extra cluster barrier per pass)
+    SelParams lp = prm;
+    lp.lean = select_smem_bytes(prm.S) > max_dyn ? 1 : 0;
+    if (select_smem_bytes_lean(prm.S) > max_dyn)
         return fail(ADAKV_UNSUPPORTED, "selection: too many segments (KV groups) per problem for shared memory");
     int cache_keys = 0;
     for (int c = int(want < 1 ? 1 : (want < kMaxSelCS ? want : kMaxSelCS)); c >= 1; --c) {
-        if (select_fit(key64, c, select_launch_smem(key64, prm, c, max_dyn, &cache_keys)) >= P) {
+        if (select_fit(key64, c, select_launch_smem(key64, lp, c, max_dyn, &cache_keys)) >= P) {
             CS = c;
             break;
         }
     }
     if (const char* e = std::getenv("ADAKV_SELECT_CS")) CS = std::max(1, std::min(kMaxSelCS, std::atoi(e)));
-    const size_t smem = select_launch_smem(key64, prm, CS, max_dyn, &cache_keys);
-    SelParams lp = prm;
+    const size_t smem = select_launch_smem(key64, lp, CS, max_dyn, &cache_keys);
     lp.cache_keys = cache_keys;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(P * CS));

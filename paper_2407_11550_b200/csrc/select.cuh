@@ -22,6 +22,8 @@ struct SelParams {
     int64_t kept_stride;
     uint32_t* err;
     int cache_keys;            // set by launch_select: each CTA's key slice lives in shared memory
+    int lean;                  // set by launch_select for many segments: one histogram buffer (an
+                               // extra cluster barrier per pass) and no kept first-digit histogram
 };
 
 adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStream_t stream);
