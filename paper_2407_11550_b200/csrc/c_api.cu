@@ -466,6 +466,7 @@ static adakv_status compress_impl(adakv_dtype dtype, const adakv_layer_shape* sh
         prm.totals = L.totals;
     }
     prm.scores = scores;
+    prm.nonneg = 1;  // window scores: means of softmax probabilities, +0 or positive
     prm.budgets = budgets;
     prm.keep = keep;
     prm.kept_pos = L.kept_pos;

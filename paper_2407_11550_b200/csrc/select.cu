@@ -52,6 +52,7 @@ template <> struct KeyOf<float> {
         if (b == 0x80000000u) b = 0u;  // -0 == +0 (the reference compares with !=, >)
         return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
     }
+    __device__ static uint32_t bits(float x) { return __float_as_uint(x); }
 };
 template <> struct KeyOf<double> {
     using type = unsigned long long;
@@ -61,6 +62,7 @@ template <> struct KeyOf<double> {
         if (b == 0x8000000000000000ull) b = 0ull;
         return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
     }
+    __device__ static unsigned long long bits(double x) { return static_cast<unsigned long long>(__double_as_longlong(x)); }
 };
 
 struct BinPick {
@@ -103,10 +105,16 @@ __device__ __forceinline__ BinPick find_bin(const uint32_t* h, int64_t krem, int
     return {bin, cum};
 }
 
-template <class F>
+// NONNEG: all scores are +0 or positive (SelParams::nonneg), so a score's bit pattern already
+// orders as its value and the order-preserving key transform is skipped (~20% of the scans)
+template <class F, bool NONNEG>
 __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams prm, unsigned long long* dbg) {
     using KT = typename KeyOf<F>::type;
     constexpr int kBits = KeyOf<F>::kBits;
+    auto kget = [](F x) -> KT {
+        if constexpr (NONNEG) return KeyOf<F>::bits(x);
+        else return KeyOf<F>::get(x);
+    };
     cg::cluster_group cluster = cg::this_cluster();
     const unsigned CS = cluster.num_blocks();
     const unsigned rank = cluster.block_rank();
@@ -188,7 +196,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         const int64_t len = hi - lo;
         const int64_t mis = int64_t(reinterpret_cast<uintptr_t>(src) / sizeof(F)) % V;
         const int64_t h0 = min(len, (V - mis) % V);
-        for (int64_t i = tid; i < h0; i += kSelThreads) kc[i] = KeyOf<F>::get(src[i]);
+        for (int64_t i = tid; i < h0; i += kSelThreads) kc[i] = kget(src[i]);
         const int64_t nv = (len - h0) / V;
         const uint4* vs = reinterpret_cast<const uint4*>(src + h0);
         for (int64_t t0 = tid; t0 < nv; t0 += 4 * kSelThreads) {
@@ -205,7 +213,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                 const F* f = reinterpret_cast<const F*>(&r[u]);
                 KT kk[V];
 #pragma unroll
-                for (int c = 0; c < V; ++c) kk[c] = KeyOf<F>::get(f[c]);
+                for (int c = 0; c < V; ++c) kk[c] = kget(f[c]);
                 if (h0 == 0) {
                     *reinterpret_cast<uint4*>(kc + t * V) = *reinterpret_cast<const uint4*>(kk);
                 } else {
@@ -214,9 +222,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                 }
             }
         }
-        for (int64_t i = h0 + nv * V + tid; i < len; i += kSelThreads) kc[i] = KeyOf<F>::get(src[i]);
+        for (int64_t i = h0 + nv * V + tid; i < len; i += kSelThreads) kc[i] = kget(src[i]);
     }
-    auto key_at = [&](int64_t e) -> KT { return cached ? kc[e - lo] : KeyOf<F>::get(sc[e]); };
+    auto key_at = [&](int64_t e) -> KT { return cached ? kc[e - lo] : kget(sc[e]); };
     // Uncached slices (too large for shared memory): every key of [a, b) from global memory
     // (L2) through fn(e, key), 16-byte loads with four per thread in flight; the unaligned
     // head and tail elements are read singly so no load leaves [a, b).
@@ -226,8 +234,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
         const int64_t va = min(b, a + (V - mis) % V);  // first vector-aligned element
         const int64_t nv = (b - va) / V;
         const int64_t vb = va + nv * V;
-        for (int64_t e = a + tid; e < va; e += kSelThreads) fn(e, KeyOf<F>::get(sc[e]));
-        for (int64_t e = vb + tid; e < b; e += kSelThreads) fn(e, KeyOf<F>::get(sc[e]));
+        for (int64_t e = a + tid; e < va; e += kSelThreads) fn(e, kget(sc[e]));
+        for (int64_t e = vb + tid; e < b; e += kSelThreads) fn(e, kget(sc[e]));
         const uint4* vs = reinterpret_cast<const uint4*>(sc + va);
         for (int64_t t0 = tid; t0 < nv; t0 += 4 * kSelThreads) {
             uint4 r[4];
@@ -242,7 +250,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(const SelParams 
                 if (t >= nv) break;
                 const F* f = reinterpret_cast<const F*>(&r[u]);
 #pragma unroll
-                for (int c = 0; c < V; ++c) fn(va + t * V + c, KeyOf<F>::get(f[c]));
+                for (int c = 0; c < V; ++c) fn(va + t * V + c, kget(f[c]));
             }
         }
     };
@@ -813,31 +821,34 @@ constexpr size_t kSelSmemCap = 220 * 1024;  // dynamic shared memory budget per 
 // The kernels' attributes are set once per device, to the most dynamic shared memory the
 // device allows beside their static shared memory (and non-portable cluster sizes), so no
 // launch ever changes them (concurrent launches of different sizes cannot race).
-template <class F>
-static cudaError_t select_prepare(size_t* max_dyn) {
+using SelKernel = void (*)(const SelParams, unsigned long long*);
+static SelKernel select_fn(bool key64, bool nonneg) {
+    return key64 ? (nonneg ? select_kernel<double, true> : select_kernel<double, false>)
+                 : (nonneg ? select_kernel<float, true> : select_kernel<float, false>);
+}
+
+static cudaError_t select_prepare(SelKernel fn, size_t* max_dyn) {
     static std::mutex mu;
-    static size_t cap[64] = {};
+    static std::map<std::pair<int, SelKernel>, size_t> cap;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lock(mu);
-    if (dev < 64 && cap[dev]) {
-        *max_dyn = cap[dev];
+    auto it = cap.find({dev, fn});
+    if (it != cap.end()) {
+        *max_dyn = it->second;
         return cudaSuccess;
     }
     cudaFuncAttributes fa{};
     int optin = 0;
-    e = cudaFuncGetAttributes(&fa, select_kernel<F>);
+    e = cudaFuncGetAttributes(&fa, fn);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const size_t c = std::min(kSelSmemCap, size_t(optin) - fa.sharedSizeBytes);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(select_kernel<F>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(select_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(c));
-    if (e == cudaSuccess && dev < 64) cap[dev] = c;
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(c));
+    if (e == cudaSuccess) cap[{dev, fn}] = c;
     *max_dyn = c;
     return e;
-}
-static cudaError_t select_prepare(bool key64, size_t* max_dyn) {
-    return key64 ? select_prepare<double>(max_dyn) : select_prepare<float>(max_dyn);
 }
 
 // dynamic shared memory of a select launch with CS CTAs per cluster; sets cache_keys
@@ -849,18 +860,18 @@ static size_t select_launch_smem(bool key64, const SelParams& prm, int CS, size_
 }
 
 // clusters of CS CTAs (smem bytes each) the device holds at once
-static int select_fit(bool key64, int CS, size_t smem) {
+static int select_fit(SelKernel fn, int CS, size_t smem) {
     static std::mutex mu;
-    static std::map<std::tuple<int, bool, int, size_t>, int> memo;
+    static std::map<std::tuple<int, SelKernel, int, size_t>, int> memo;
     int dev = 0;
     cudaGetDevice(&dev);
-    const auto key = std::make_tuple(dev, key64, CS, smem);
+    const auto key = std::make_tuple(dev, fn, CS, smem);
     std::lock_guard<std::mutex> lock(mu);
     auto it = memo.find(key);
     if (it != memo.end()) return it->second;
     int n = 0;
     size_t max_dyn = 0;
-    if (select_prepare(key64, &max_dyn) == cudaSuccess) {
+    if (select_prepare(fn, &max_dyn) == cudaSuccess) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(unsigned(CS));
         cfg.blockDim = dim3(kSelThreads);
@@ -872,9 +883,7 @@ static int select_fit(bool key64, int CS, size_t smem) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (key64 ? cudaOccupancyMaxActiveClusters(&n, select_kernel<double>, &cfg) != cudaSuccess
-                  : cudaOccupancyMaxActiveClusters(&n, select_kernel<float>, &cfg) != cudaSuccess)
-            n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) n = 0;
     }
     cudaGetLastError();
     memo[key] = n;
@@ -891,8 +900,9 @@ adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStre
     const int64_t per_cta = 16384;
     const int64_t want = ceil_div(prm.N, per_cta);
     int CS = int(want < 1 ? 1 : (want > 8 ? 8 : want));
+    const SelKernel fn = select_fn(key64, prm.nonneg != 0);
     size_t max_dyn = 0;
-    ADAKV_CUDA_TRY(select_prepare(key64, &max_dyn));
+    ADAKV_CUDA_TRY(select_prepare(fn, &max_dyn));
     // per-segment histograms (~4.75 KB per segment) beside the per-warp ones fit up to 39
     // segments (KV groups) per problem on B200; more take the lean layout (~2.75 KB per
     // segment, up to 68: one histogram buffer and an extra cluster barrier per pass)
@@ -902,7 +912,7 @@ adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStre
         return fail(ADAKV_UNSUPPORTED, "selection: too many segments (KV groups) per problem for shared memory");
     int cache_keys = 0;
     for (int c = int(want < 1 ? 1 : (want < kMaxSelCS ? want : kMaxSelCS)); c >= 1; --c) {
-        if (select_fit(key64, c, select_launch_smem(key64, lp, c, max_dyn, &cache_keys)) >= P) {
+        if (select_fit(fn, c, select_launch_smem(key64, lp, c, max_dyn, &cache_keys)) >= P) {
             CS = c;
             break;
         }
@@ -922,8 +932,7 @@ adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStre
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (key64) ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel<double>, lp, g_sel_dbg));
-    else ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel<float>, lp, g_sel_dbg));
+    ADAKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, lp, g_sel_dbg));
     return ADAKV_OK;
 }
 

@@ -24,6 +24,8 @@ struct SelParams {
     int cache_keys;            // set by launch_select: each CTA's key slice lives in shared memory
     int lean;                  // set by launch_select for many segments: one histogram buffer (an
                                // extra cluster barrier per pass) and no kept first-digit histogram
+    int nonneg;                // every score is +0 or positive (adakv_compress's window scores):
+                               // the bit patterns order as the values, no key transform needed
 };
 
 adakv_status launch_select(bool key64, int64_t P, const SelParams& prm, cudaStream_t stream);
