@@ -356,6 +356,24 @@ adakv_status adakv_compact_rows_f64(int64_t segments, const uint8_t* mask, const
                                     const double* src_v, int64_t d, const int64_t* out_off, double* dst_k,
                                     double* dst_v, adakv_stream_t stream);
 
+/* ----------------------------------------------------------------------------
+ * KV-group sharding glue (sharding.py; no single reference counterpart: the
+ * layer-wide top-B of adaptive_allocation, budget.hpp:118-140, with the KV
+ * groups of a layer spread over ranks).
+ * adakv_shard_pack_candidates: this rank's ONE all-gather payload, int32
+ *   [local_groups + 2k] = [counts | f32 bits of the k candidate scores | positions],
+ *   from scores [local_groups, outside] f32 and the local top-k (counts per group,
+ *   positions segment-major ascending), all DEVICE.
+ * adakv_shard_build_union: gathered [world, local_groups + 2k] -> union [world *
+ *   local_groups, slots] f32: each group's candidate scores in position order, -1
+ *   (below every score) in the empty slots.
+ * ------------------------------------------------------------------------- */
+adakv_status adakv_shard_pack_candidates(const float* scores, const int32_t* counts, const int32_t* pos,
+                                         int64_t local_groups, int64_t outside, int64_t k, int32_t* payload,
+                                         adakv_stream_t stream);
+adakv_status adakv_shard_build_union(const int32_t* gathered, int64_t world, int64_t local_groups, int64_t k,
+                                     int64_t slots, float* out, adakv_stream_t stream);
+
 /* Device memory helpers so C/C++ callers need nothing but this header (synchronous). */
 adakv_status adakv_device_malloc(void** ptr, size_t bytes);
 adakv_status adakv_device_free(void* ptr);

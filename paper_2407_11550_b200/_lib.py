@@ -87,6 +87,8 @@ def _sig(L):
     L.adakv_compress.argtypes = [S, C.POINTER(LayerShape), C.POINTER(PolicyConfig), I64, VP, VP, VP, VP, I64,
                                  VP, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP]
     L.adakv_compress_split.argtypes = L.adakv_compress.argtypes + [VP]
+    L.adakv_shard_pack_candidates.argtypes = [VP, VP, VP, I64, I64, I64, VP, VP]
+    L.adakv_shard_build_union.argtypes = [VP, I64, I64, I64, I64, VP, VP]
     L.adakv_compress_workspace.argtypes = [S, C.POINTER(LayerShape), C.POINTER(PolicyConfig), PSZ]
     L.adakv_cache_rows.argtypes = [C.POINTER(LayerShape), I64, VP, I64]
     L.adakv_cache_rows.restype = I64

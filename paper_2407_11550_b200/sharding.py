@@ -118,12 +118,8 @@ def kv_group_sharded_allocation(local_scores: torch.Tensor, g0: int, G: int, tot
     # 1) local top-k candidates (same kernel as the single-GPU path)
     k_local = min(int(total), G_local * n_o)
     counts, pos = selector.topk(local_scores, k_local)
-    flat = local_scores.reshape(-1).float()
-    gidx = torch.repeat_interleave(torch.arange(G_local, device=dev), counts.to(torch.int64),
-                                   output_size=k_local) if k_local else torch.zeros(0, dtype=torch.int64, device=dev)
-    cand = flat[gidx * n_o + pos.to(torch.int64)]
     # 2) one all-gather of a fixed-size payload: [counts | score bits | positions]
-    payload = torch.cat([counts.to(torch.int32), cand.view(torch.int32), pos.to(torch.int32)])
+    payload = (_cuda_pack if local_scores.is_cuda else _torch_pack)(local_scores, counts, pos, k_local)
     if dist.is_initialized():  # (also at world size 1: the same NCCL path the ranks take)
         if dist.get_backend(group) == "nccl":
             gathered = torch.empty((world, payload.numel()), dtype=torch.int32, device=dev)
@@ -136,14 +132,7 @@ def kv_group_sharded_allocation(local_scores: torch.Tensor, g0: int, G: int, tot
         gathered = payload.reshape(1, -1)
     # 3) union [G, S] ordered by (group, position); empty slots -1 (below every score >= 0)
     S = max(1, min(k_local, n_o))
-    g_counts = gathered[:, :G_local].reshape(-1).to(torch.int64)            # [G] (rank-major = group order)
-    g_scores = gathered[:, G_local:G_local + k_local].contiguous().view(torch.float32)  # [world, k_local]
-    g_start = (torch.cumsum(g_counts.view(world, G_local), 1) - g_counts.view(world, G_local)).reshape(-1)
-    j = torch.arange(S, device=dev)
-    valid = j[None, :] < g_counts[:, None]                                   # [G, S]
-    src = (g_start[:, None] + j[None, :]).clamp(max=max(k_local - 1, 0))     # index within the rank's list
-    rank_of = torch.arange(G, device=dev) // G_local
-    union = torch.where(valid, g_scores[rank_of[:, None], src], torch.full((), -1.0, device=dev))
+    union = (_cuda_union if gathered.is_cuda else _torch_union)(gathered, world, G_local, k_local, S)
     raw, budgets = selector.allocate(union.float(), int(total), float(alpha), blend)
     # 4) this rank's groups with the merged budgets
     kept_pos = selector.given(local_scores, budgets[g0:g0 + G_local])
@@ -186,6 +175,59 @@ def compress_kv_group_sharded(q, k, v, layer_budget: int, G: int, *, g0: int, gr
                                  p(alloc.kept_pos), max(int(alloc.kept_pos.numel()), 1), int(reserve), p(out.k),
                                  p(out.v), p(out.seg_start), p(out.seqlens), p(out.seg_cap), None, ops._stream()))
     return out, alloc
+
+
+def _torch_pack(local_scores, counts, pos, k):
+    """The all-gather payload [counts | candidate score bits | positions] with torch ops (CPU path)."""
+    G_local, n_o = local_scores.shape
+    dev = local_scores.device
+    flat = local_scores.reshape(-1).float()
+    gidx = torch.repeat_interleave(torch.arange(G_local, device=dev), counts.to(torch.int64),
+                                   output_size=k) if k else torch.zeros(0, dtype=torch.int64, device=dev)
+    cand = flat[gidx * n_o + pos.to(torch.int64)]
+    return torch.cat([counts.to(torch.int32), cand.view(torch.int32), pos.to(torch.int32)])
+
+
+def _torch_union(gathered, world, G_local, k, S):
+    """The [world G_local, S] candidate union with torch ops (CPU path)."""
+    dev = gathered.device
+    G = world * G_local
+    g_counts = gathered[:, :G_local].reshape(-1).to(torch.int64)                 # [G] (rank-major = group order)
+    g_scores = gathered[:, G_local:G_local + k].contiguous().view(torch.float32)  # [world, k]
+    g_start = (torch.cumsum(g_counts.view(world, G_local), 1) - g_counts.view(world, G_local)).reshape(-1)
+    j = torch.arange(S, device=dev)
+    valid = j[None, :] < g_counts[:, None]                                        # [G, S]
+    src = (g_start[:, None] + j[None, :]).clamp(max=max(k - 1, 0))                # index within the rank's list
+    rank_of = torch.arange(G, device=dev) // G_local
+    return torch.where(valid, g_scores[rank_of[:, None], src], torch.full((), -1.0, device=dev))
+
+
+def _cuda_pack(local_scores, counts, pos, k):
+    """adakv_shard_pack_candidates: the all-gather payload in one kernel."""
+    import ctypes as C
+    from . import _lib as L
+    from . import ops
+    G_local, n_o = local_scores.shape
+    sc = local_scores.float().contiguous()
+    cnt = counts.to(torch.int32).contiguous()
+    ps = pos.to(torch.int32).contiguous()
+    payload = torch.empty(G_local + 2 * k, dtype=torch.int32, device=local_scores.device)
+    L.check(L.lib().adakv_shard_pack_candidates(C.c_void_p(sc.data_ptr()), C.c_void_p(cnt.data_ptr()),
+                                                C.c_void_p(ps.data_ptr()) if k else None, G_local, n_o, k,
+                                                C.c_void_p(payload.data_ptr()), ops._stream()))
+    return payload
+
+
+def _cuda_union(gathered, world, G_local, k, S):
+    """adakv_shard_build_union: the [G, S] candidate union in one kernel."""
+    import ctypes as C
+    from . import _lib as L
+    from . import ops
+    g = gathered.to(torch.int32).contiguous()
+    union = torch.empty((world * G_local, S), dtype=torch.float32, device=gathered.device)
+    L.check(L.lib().adakv_shard_build_union(C.c_void_p(g.data_ptr()), world, G_local, k, S,
+                                            C.c_void_p(union.data_ptr()), ops._stream()))
+    return union
 
 
 def pack_candidate_bytes(k: int, G_local: int) -> int:

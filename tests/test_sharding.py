@@ -169,3 +169,28 @@ def test_kv_group_sharded_compress_nccl_world1(dev, oracle_mod, capfd):
             dist.destroy_process_group()
     err = capfd.readouterr()
     print("\n".join(l for l in (err.out + err.err).splitlines() if "NCCL INFO" in l and ("comm" in l or "Init" in l))[:2000])
+
+
+@pytest.mark.gpu
+def test_shard_glue_kernels_match_torch_glue(dev):
+    """adakv_shard_pack_candidates / adakv_shard_build_union (the sharded path's device glue)
+    equal the torch formulation the CPU tests run, for three ranks' payloads with ragged
+    per-group counts (including empty groups) and heavy ties."""
+    from paper_2407_11550_b200.sharding import CudaSelector, _cuda_pack, _cuda_union, _torch_pack, _torch_union
+    sel = CudaSelector()
+    G_local, n_o, k, world = 2, 300, 250, 3
+    payloads = []
+    for r in range(world):
+        s = torch.as_tensor(_scores(30 + r, G_local, n_o, "ties"), device=dev)
+        if r == 1:
+            s[1] = 0.0  # one group with no candidate above the others
+        counts, pos = sel.topk(s, k)
+        pc = _cuda_pack(s, counts, pos, k)
+        pt = _torch_pack(s.cpu(), counts.cpu(), pos.cpu(), k)
+        assert torch.equal(pc.cpu(), pt), r
+        payloads.append(pc)
+    gathered = torch.stack(payloads)
+    S = min(k, n_o)
+    uc = _cuda_union(gathered, world, G_local, k, S)
+    ut = _torch_union(gathered.cpu(), world, G_local, k, S)
+    assert torch.equal(uc.cpu().view(torch.int32), ut.view(torch.int32))
