@@ -1,0 +1,83 @@
+"""Seeded random sweep of the whole path on the device: random shapes (problems, KV groups,
+group sizes 1-8, window, prompt, head dim 64/128), pool kernels, kinds and budgets, through
+adakv_compress (tcgen05 scoring where the shape allows it, the SIMT kernels otherwise) and
+one decode step with its append.  Per case:
+  * the oracle's selection (budget.hpp:118-158, policies.hpp:80-93, 178-196) fed the device's
+    own scores reproduces budgets and keep masks bit-exactly, and the cache holds exactly the
+    kept rows then the window rows of every group (policies.hpp:273-290);
+  * the decode output is within the bf16 tolerance of the fp64 attention over those rows plus
+    the appended one (attention.hpp:169-196), and the appended row lands at the segment end.
+48 cases by default (ADAKV_FUZZ_CASES: 300 measured green).
+"""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2407_11550_b200 as A  # noqa: E402
+from paper_2407_11550_b200.synthetic import planted_layer  # noqa: E402
+
+
+def _case(seed):
+    rng = np.random.default_rng(seed)
+    P = int(rng.integers(1, 4))
+    G = int(rng.choice([1, 2, 3, 4, 5, 8, 13]))
+    g = int(rng.choice([1, 2, 3, 4, 6, 8]))
+    m = int(rng.choice([4, 8, 32, 32]))
+    d = int(rng.choice([64, 128, 128]))
+    n_o = int(rng.integers(m + 1, 1200))
+    pool = int(rng.choice([1, 3, 5, 7]))
+    kind = str(rng.choice(["ada_snapkv", "ada_snapkv", "snapkv"]))
+    lb = int(rng.integers(m * G + G, G * (n_o + m) + 1))
+    return P, G, g, m, d, n_o, pool, kind, lb
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("ADAKV_FUZZ_CASES", "48"))))
+def test_random_compress_then_decode(dev, oracle_mod, seed):
+    O = oracle_mod
+    P, G, g, m, d, n_o, pool, kind, lb = _case(seed)
+    H = G * g
+    q, k, v = planted_layer(P, H, G, n_o, m, d, seed=100 + seed, dtype=torch.bfloat16, device=dev)
+    c = A.compress(q, k, v, lb, kind=kind, pool_kernel=pool, alpha=0.2, reserve=2, return_scores=True,
+                   return_keep=True, check=True)
+    outside = lb - m * G
+    kk, vv = k.cpu(), v.cpu()
+    for p in range(P):
+        s64 = c.scores[p].double().cpu().numpy()
+        caps = np.full(G, n_o)
+        if kind == "ada_snapkv":
+            raw = O.adaptive_allocation(list(s64), outside)
+            b = O.repair_zero_budgets(O.safeguard_blend(raw, outside, G, 0.2, caps), caps)
+        else:
+            b = O.repair_zero_budgets(O.uniform_allocation(outside, G, caps), caps)
+        keep = np.stack([O.topk_decision(s64[i], int(b[i])) for i in range(G)])
+        assert c.budgets[p * G:(p + 1) * G].cpu().tolist() == b.tolist(), (seed, p)
+        assert np.array_equal(c.keep[p].cpu().numpy(), keep), (seed, p)
+        for i in range(G):
+            idx = np.concatenate([np.nonzero(keep[i])[0], n_o + np.arange(m)])
+            kr, vr = c.segment(p, i)
+            assert torch.equal(kr.cpu().view(torch.int16), kk[p, i, idx].view(torch.int16)), (seed, p, i)
+            assert torch.equal(vr.cpu().view(torch.int16), vv[p, i, idx].view(torch.int16)), (seed, p, i)
+    # one decode step with its append, against fp64 attention over the retained rows + the new one
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    qd = torch.randn((P, H, d), generator=gen, device=dev).to(torch.bfloat16)
+    kn = torch.randn((P, G, d), generator=gen, device=dev).to(torch.bfloat16)
+    vn = torch.randn((P, G, d), generator=gen, device=dev).to(torch.bfloat16)
+    before = c.seqlens.clone()
+    o = A.decode(qd, c, kn, vn, check=True)
+    assert torch.equal(c.seqlens, before + 1)
+    for p in range(P):
+        for i in range(G):
+            kr, vr = c.segment(p, i)
+            assert torch.equal(kr[-1].view(torch.int16), kn[p, i].view(torch.int16))
+            assert torch.equal(vr[-1].view(torch.int16), vn[p, i].view(torch.int16))
+            kr64, vr64 = kr.double(), vr.double()
+            for h in range(i * g, (i + 1) * g):
+                w = torch.softmax(kr64 @ qd[p, h].double() / d ** 0.5, dim=0)
+                ref = w @ vr64
+                err = (o[p, h].double() - ref).abs().max().item()
+                assert err <= 2e-2 and err <= 1e-2 * max(ref.abs().max().item(), 1e-3) + 4e-3, (seed, p, h, err)
