@@ -81,3 +81,37 @@ def test_random_compress_then_decode(dev, oracle_mod, seed):
                 ref = w @ vr64
                 err = (o[p, h].double() - ref).abs().max().item()
                 assert err <= 2e-2 and err <= 1e-2 * max(ref.abs().max().item(), 1e-3) + 4e-3, (seed, p, h, err)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("ADAKV_FUZZ_SELECT_CASES", "24"))))
+def test_random_segmented_select(dev, oracle_mod, seed):
+    """Random selection problems straight through adakv_segmented_select: 1-40 problems, 1-64
+    ragged non-empty segments (the lean layout past 39), up to ~600K keys per problem (clusters
+    of up to 16 CTAs, slices streamed from L2), heavy ties, f32 or f64 keys, adaptive (blended,
+    repaired) or uniform allocation -- budgets and keep masks bit-exact to evict_rows
+    (policies.hpp:298-323), kept positions in flat order."""
+    O = oracle_mod
+    rng = np.random.default_rng(1000 + seed)
+    P = int(rng.integers(1, 41)) if seed % 3 else 1
+    S = int(rng.choice([1, 2, 5, 8, 16, 39, 40, 64]))
+    big = seed % 4 == 0
+    sizes = rng.integers(1, (600000 // S) if big else 3000, size=S)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    N = int(off[-1])
+    levels = int(rng.choice([8, 64, 4096]))
+    x = np.floor(rng.random((P, N)) * levels) / levels
+    dt = torch.float64 if seed % 5 == 0 else torch.float32
+    s = torch.as_tensor(x, dtype=dt, device=dev)
+    adaptive = bool(seed % 2 == 0)
+    total = int(rng.integers(S, N + 1))
+    r = A.segmented_select(s, off, total, "adaptive" if adaptive else "uniform", blend=adaptive, alpha=0.2,
+                           repair=True)
+    for p in range(min(P, 3)):
+        rows = [x[p, off[i]:off[i + 1]] for i in range(S)]
+        alloc, keep = O.evict_rows(rows, total, adaptive, 0.2)
+        assert r["budgets"][p].cpu().tolist() == alloc.tolist(), (seed, p)
+        kp = np.concatenate(keep)
+        assert np.array_equal(r["keep"][p].cpu().numpy(), kp), (seed, p)
+        pos = np.concatenate([np.nonzero(k)[0] for k in keep])
+        assert np.array_equal(r["kept_pos"][p, :total].cpu().numpy(), pos), (seed, p)
+    A.workspace_status(r["ws"])
