@@ -115,3 +115,64 @@ def test_random_segmented_select(dev, oracle_mod, seed):
         pos = np.concatenate([np.nonzero(k)[0] for k in keep])
         assert np.array_equal(r["kept_pos"][p, :total].cpu().numpy(), pos), (seed, p)
     A.workspace_status(r["ws"])
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("ADAKV_FUZZ_GENERIC_CASES", "16"))))
+def test_random_generic_dtypes_and_kinds(dev, oracle_mod, seed):
+    """The SIMT paths: f32 / f64 layers (scores from the generic kernels, decode on the generic
+    split-K kernel), every kind including StreamingLLM and per-problem (pyramid) budgets,
+    optionally with V in pinned host memory -- selection bit-exact on the device's own scores,
+    retained rows exact, decode within fp32 / fp64 tolerance of fp64 attention."""
+    O = oracle_mod
+    rng = np.random.default_rng(5000 + seed)
+    dt = torch.float64 if seed % 2 else torch.float32
+    P = int(rng.integers(1, 4))
+    G = int(rng.choice([1, 2, 3, 4, 8]))
+    g = int(rng.choice([1, 2, 4]))
+    m = int(rng.choice([2, 8, 16]))
+    d = int(rng.choice([16, 64, 128]))
+    n_o = int(rng.integers(m + 1, 700))
+    pool = int(rng.choice([1, 3, 5, 7, 9]))
+    kind = str(rng.choice(["ada_snapkv", "snapkv", "streaming_llm", "ada_pyramid"]))
+    H = G * g
+    q, k, v = planted_layer(P, H, G, n_o, m, d, seed=200 + seed, dtype=dt, device=dev)
+    lb_per = rng.integers(m * G + G, G * (n_o + m) + 1, size=P)
+    per_problem = kind == "ada_pyramid"
+    lb = int(lb_per[0])
+    vin = v.cpu().pin_memory() if seed % 3 == 0 else v
+    c = A.compress(q, k, vin, lb, kind=kind, pool_kernel=pool, alpha=0.2, reserve=1, return_scores=True,
+                   return_keep=True, check=True,
+                   layer_budgets=torch.as_tensor(lb_per, device=dev) if per_problem else None)
+    kk, vv = k.cpu(), v.cpu()
+    for p in range(P):
+        outside = int(lb_per[p] if per_problem else lb) - m * G
+        s64 = c.scores[p].double().cpu().numpy()
+        caps = np.full(G, n_o)
+        if kind in ("ada_snapkv", "ada_pyramid"):
+            raw = O.adaptive_allocation(list(s64), outside)
+            b = O.repair_zero_budgets(O.safeguard_blend(raw, outside, G, 0.2, caps), caps)
+        else:
+            b = O.repair_zero_budgets(O.uniform_allocation(outside, G, caps), caps)
+        if kind == "streaming_llm":
+            keep = np.stack([O.streaming_llm_decision(n_o, min(4, int(x)), int(x) - min(4, int(x))) for x in b])
+        else:
+            keep = np.stack([O.topk_decision(s64[i], int(b[i])) for i in range(G)])
+        assert c.budgets[p * G:(p + 1) * G].cpu().tolist() == b.tolist(), (seed, p)
+        assert np.array_equal(c.keep[p].cpu().numpy(), keep), (seed, p)
+        for i in range(G):
+            idx = np.concatenate([np.nonzero(keep[i])[0], n_o + np.arange(m)])
+            kr, vr = c.segment(p, i)
+            assert torch.equal(kr.cpu(), kk[p, i, idx]) and torch.equal(vr.cpu(), vv[p, i, idx]), (seed, p, i)
+    qd = torch.as_tensor(rng.normal(size=(P, H, d)), dtype=dt, device=dev)
+    kn = torch.as_tensor(rng.normal(size=(P, G, d)), dtype=dt, device=dev)
+    vn = torch.as_tensor(rng.normal(size=(P, G, d)), dtype=dt, device=dev)
+    o = A.decode(qd, c, kn, vn, check=True)
+    tol = 1e-10 if dt == torch.float64 else 2e-5
+    for p in range(P):
+        for i in range(G):
+            kr, vr = c.segment(p, i)
+            for h in range(i * g, (i + 1) * g):
+                w = torch.softmax(kr.double() @ qd[p, h].double() / d ** 0.5, dim=0)
+                ref = w @ vr.double()
+                err = (o[p, h].double() - ref).abs().max().item()
+                assert err <= tol * max(1.0, ref.abs().max().item()), (seed, p, h, err)
