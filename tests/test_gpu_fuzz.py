@@ -176,3 +176,28 @@ def test_random_generic_dtypes_and_kinds(dev, oracle_mod, seed):
                 ref = w @ vr.double()
                 err = (o[p, h].double() - ref).abs().max().item()
                 assert err <= tol * max(1.0, ref.abs().max().item()), (seed, p, h, err)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("ADAKV_FUZZ_SHARD_CASES", "12"))))
+def test_random_kv_group_sharded_compress_matches_compress(dev, seed):
+    """The KV-group-sharded compress (local top-k, the device-packed payload, the candidate union,
+    the merged allocation, the per-group selection; world size 1) equals the single-GPU compress
+    on random shapes: budgets, segment lengths and every retained row bit for bit."""
+    from paper_2407_11550_b200.sharding import compress_kv_group_sharded
+    rng = np.random.default_rng(7000 + seed)
+    G = int(rng.choice([1, 2, 4, 8]))
+    g = int(rng.choice([1, 2, 4, 8]))
+    m, d = 32, 128
+    n_o = int(rng.integers(64, 3000))
+    H = G * g
+    q, k, v = planted_layer(1, H, G, n_o, m, d, seed=300 + seed, dtype=torch.bfloat16, device=dev)
+    lb = int(rng.integers(m * G + G, G * (n_o + m) + 1))
+    ref = A.compress(q, k, v, lb, reserve=2)
+    sh, _ = compress_kv_group_sharded(q[0], k[0], v[0], lb, G, g0=0, reserve=2)
+    assert torch.equal(sh.budgets.cpu(), ref.budgets.cpu()), seed
+    assert torch.equal(sh.seqlens.cpu(), ref.seqlens.cpu()), seed
+    for i in range(G):
+        kr, vr = ref.segment(0, i)
+        ks, vs = sh.segment(0, i)
+        assert torch.equal(ks.view(torch.int16), kr.view(torch.int16)), (seed, i)
+        assert torch.equal(vs.view(torch.int16), vr.view(torch.int16)), (seed, i)
